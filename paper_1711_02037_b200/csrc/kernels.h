@@ -1,0 +1,138 @@
+// kernels.h — host-side launch wrappers of the rnmf-b200 sm_100a kernels.
+// Every wrapper enqueues on `stream` and returns the number of kernels it launched.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rnmf_gpu {
+
+// ---- validation / mean / norm pass over X (kernels_scan.cu) ---------------------------------
+// out[0] = sum(X), out[1] = sum(X^2) (fp64, fixed-order reduction).  bad[0] = linear index of
+// the first non-finite entry, bad[1] = of the first negative entry (UINT64_MAX if none).
+// `part` must hold 2 * scan_grid() doubles.
+int scan_grid();
+template <typename T>
+int launch_scan(const T* x, int64_t count, unsigned long long* bad, double* part, double* out,
+                cudaStream_t stream);
+
+// ---- X-streaming GEMMs (kernels_xgemm.cu) ----------------------------------------------------
+// Y (m x c) = X (m x n) * S (n x c).  All row-major, leading dims = column counts.
+template <typename T>
+int launch_xw(const T* x, int64_t m, int64_t n, const T* s, int c, T* y, cudaStream_t stream);
+
+// Fused full-space metrics pass 1 over X: with S = H^T (n x k) and W (m x k):
+//   part_obj[b]  = partial sum of (X - W H)^2 over CTA b's rows
+//   part_pgw[b]  = partial sum of projected (grad_W)^2, grad_W = -2 (X H^T - W (H H^T))
+// hht: k x k fp64.  Returns launches; *nblocks receives the number of partials written.
+template <typename T>
+int launch_xw_metrics(const T* x, int64_t m, int64_t n, const T* ht, const T* w, int k,
+                      const double* hht, double* part_obj, double* part_pgw, int* nblocks,
+                      cudaStream_t stream);
+int xw_metrics_blocks(int64_t m);
+
+// P (n x c) = X^T (n x m) * S (m x c), split over m into `splits` partial sums (part holds
+// splits * n * c values of T), then reduced in fixed order into `out` (n x c, or c x n when
+// transpose_out).  splits = 0 picks a default.
+template <typename T>
+int launch_xtw(const T* x, int64_t m, int64_t n, const T* s, int c, T* part, int splits, T* out,
+               bool transpose_out, cudaStream_t stream);
+int xtw_default_splits(int64_t m, int64_t n);
+
+// Metrics pass 2: with S = W (m x k): part_pgh[b] = partial sums of projected (grad_H)^2,
+// grad_H = -2 (W^T X - (W^T W) H), wtw: k x k fp64.  part holds splits*n*k values of T.
+template <typename T>
+int launch_xtw_metrics(const T* x, int64_t m, int64_t n, const T* w, int k, const T* h,
+                       const double* wtw, T* part, int splits, double* part_pgh, int* nblocks,
+                       cudaStream_t stream);
+
+// ---- small dense helpers (kernels_xgemm.cu) ---------------------------------------------------
+// G (c x c, fp64) = A^T A for A (rows x c) row-major.  part: gram_parts(rows)*c*c doubles.
+template <typename T>
+int launch_gram_rows(const T* a, int64_t rows, int c, double* part, double* g, cudaStream_t stream);
+// G (c x c, fp64) = A A^T for A (c x cols) row-major.
+template <typename T>
+int launch_gram_cols(const T* a, int c, int64_t cols, double* part, double* g, cudaStream_t stream);
+int gram_parts(int64_t len);
+// out (cols x rows) = in (rows x cols)^T
+template <typename T>
+int launch_transpose(const T* in, int64_t rows, int64_t cols, T* out, cudaStream_t stream);
+// out[i] = (T)(in[i] * scale)
+template <typename T>
+int launch_scale_cast(const double* in, int64_t count, double scale, T* out, cudaStream_t stream);
+// out[i] = (double)in[i]
+template <typename T>
+int launch_widen(const T* in, int64_t count, double* out, cudaStream_t stream);
+// sum of `count` doubles in fixed order -> out[0]
+int launch_sum_parts(const double* part, int count, double* out, cudaStream_t stream);
+// writes %globaltimer to *out
+int launch_timestamp(unsigned long long* out, cudaStream_t stream);
+
+// ---- tall-skinny QR (kernels_tsqr.cu) ---------------------------------------------------------
+// Householder TSQR of A (rows x l, row-major) -> explicit thin Q (rows x l, written to q_out in
+// T).  Workspace sized by tsqr_workspace_doubles.  Requires rows >= l.
+int64_t tsqr_workspace_doubles(int64_t rows, int l, int max_smem);
+template <typename T>
+int launch_tsqr(const T* a, int64_t rows, int l, T* q_out, double* ws, int max_smem,
+                cudaStream_t stream);
+int tsqr_max_l(int max_smem);
+
+// ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cu) -----------------------------
+enum SweepFlags : int {
+  kInitWt = 1,    // W~ <- Q^T W
+  kInitWn = 2,    // wn <- diag(W^T W)
+  kEval0 = 4,     // record 0: objc0, pgrad0 (grad_h = -2 W~^T residc), T, V, E
+  kTvOnly = 8,    // T, V from the current H (no record)
+  kDoW = 16,      // W phase in each sweep
+  kDoH = 32,      // H phase (+ evaluation) in each sweep
+  kRecord = 64,   // write trace entries / stop checks
+};
+
+template <typename T>
+struct SweepArgs {
+  const T* q;  // m x l
+  const T* b;  // l x n
+  T* w;        // m x k (in/out)
+  T* h;        // k x n (in/out)
+  double* wt;  // l x k (in/out state)
+  double* wn;  // k
+  double* tm;  // l x k  (T = B H^T)
+  double* vm;  // k x k  (V = H H^T)
+  double* em;  // l x k  (E = residc H^T)
+  int64_t m, n;
+  int l, k;
+  double alpha_w, alpha_h, beta_w, beta_h;
+  int flags;
+  int64_t t_begin, t_end;  // sweeps t_begin..t_end (inclusive)
+  int stop_rule;           // RNMF_STOP_*
+  double tol;
+  double* pgrad0;          // device scalar (written by kEval0)
+  double* trace_objc;      // [max_iter + 1]
+  double* trace_pgrad;     // [max_iter + 1]
+  unsigned long long* trace_time;  // [max_iter + 1]
+  long long* status;       // [0] = last completed sweep, [1] = stopped flag
+  unsigned* barrier;       // zeroed before launch
+  double* part;            // [2 * sweep_part_len(l,k) * grid]  (two alternating slots)
+  double* fin;             // [2 * sweep_part_len(l,k)]
+};
+
+__host__ __device__ inline int64_t sweep_part_len(int l, int k) {
+  const int64_t a = 2 * int64_t(l) * k + int64_t(k) * k + 2;
+  const int64_t b = int64_t(l) * k + k;
+  const int64_t c = a > b ? a : b;
+  return c > l + 1 ? c : int64_t(l) + 1;
+}
+// Returns the cooperative grid size that will be used (0 if the problem does not fit).
+struct SweepPlan {
+  int grid = 0;
+  bool q_in_smem = false;
+  size_t smem = 0;
+  int64_t rows_per_cta = 0;
+  int64_t cols_per_cta = 0;
+};
+template <typename T>
+SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem);
+template <typename T>
+int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream);
+
+}  // namespace rnmf_gpu

@@ -1,0 +1,1079 @@
+// rnmf_gpu.cu — host orchestration of the B200 randomized-HALS path and its C ABI
+// (include/rnmf_gpu.h).  Everything numeric runs in the sm_100a kernels of kernels_*.cu; the host
+// validates arguments in the reference's order, draws the reference's random streams, sequences
+// the kernels on one CUDA stream and assembles the trace.
+#include "../../include/rnmf_gpu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace rnmf_gpu {
+
+// ---- reference exception classes (p/include/rnmf/types.hpp:22-39) ---------------------------
+struct ShapeError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct ParameterError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+static std::string shape_string(int64_t r, int64_t c) { return std::to_string(r) + "x" + std::to_string(c); }
+
+// ---- the reference random stream (p/include/rnmf/types.hpp:55-102) ---------------------------
+// Needed by the product itself: with no overrides, Omega and the initial factors must be the
+// reference's own draws.
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : seed_(seed), engine_(seed) {}
+  uint64_t seed() const { return seed_; }
+  uint64_t next_u64() { return engine_(); }
+  double uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  double gaussian() {
+    if (has_spare_) {
+      has_spare_ = false;
+      return spare_;
+    }
+    double u1 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    const double u2 = uniform();
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    const double angle = 2.0 * 3.141592653589793238462643383279502884 * u2;
+    spare_ = radius * std::sin(angle);
+    has_spare_ = true;
+    return radius * std::cos(angle);
+  }
+  Rng split(uint64_t stream) const {
+    uint64_t x = seed_ + 0x9e3779b97f4a7c15ULL * (stream + 1);
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return Rng(x ^ (x >> 31));
+  }
+
+ private:
+  uint64_t seed_;
+  std::mt19937_64 engine_;
+  double spare_ = 0.0;
+  bool has_spare_ = false;
+};
+
+constexpr uint64_t kSketchStream = 3;  // p/include/rnmf/hals.hpp:107
+
+// ---- device / pinned buffers owned by a context ----------------------------------------------
+struct Buffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace rnmf_gpu
+
+using namespace rnmf_gpu;
+
+struct rnmf_gpu_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  int max_smem = 0;
+  std::map<std::string, Buffer> dev;
+  std::map<std::string, Buffer> pinned;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+  rnmf_stage_times last{};
+
+  template <typename V>
+  V* d(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(V);
+    Buffer& b = dev[name];
+    if (b.bytes < bytes) {
+      if (b.p) RNMF_CUDA(cudaFree(b.p));
+      b.p = nullptr;
+      RNMF_CUDA(cudaMalloc(&b.p, bytes));
+      b.bytes = bytes;
+    }
+    return static_cast<V*>(b.p);
+  }
+  template <typename V>
+  V* h(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(V);
+    Buffer& b = pinned[name];
+    if (b.bytes < bytes) {
+      if (b.p) RNMF_CUDA(cudaFreeHost(b.p));
+      b.p = nullptr;
+      RNMF_CUDA(cudaMallocHost(&b.p, bytes));
+      b.bytes = bytes;
+    }
+    return static_cast<V*>(b.p);
+  }
+  cudaEvent_t event() {
+    if (event_next == event_pool.size()) {
+      cudaEvent_t e;
+      RNMF_CUDA(cudaEventCreate(&e));
+      event_pool.push_back(e);
+    }
+    return event_pool[event_next++];
+  }
+};
+
+namespace rnmf_gpu {
+
+// ---- stage timing -----------------------------------------------------------------------------
+enum Stage { kScan, kSketch, kQr, kInit, kSweeps, kMetrics, kXw, kXtw, kH2D, kD2H, kNumStages };
+
+struct Timer {
+  rnmf_gpu_context* ctx;
+  struct Span {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Span> spans;
+  cudaEvent_t start{}, stop{};
+  int64_t launches = 0;
+  explicit Timer(rnmf_gpu_context* c) : ctx(c) {
+    ctx->event_next = 0;
+    start = ctx->event();
+    RNMF_CUDA(cudaEventRecord(start, ctx->stream));
+  }
+  cudaEvent_t mark() {
+    cudaEvent_t e = ctx->event();
+    RNMF_CUDA(cudaEventRecord(e, ctx->stream));
+    return e;
+  }
+  template <typename F>
+  void span(int stage, F&& f) {
+    cudaEvent_t a = mark();
+    f();
+    cudaEvent_t b = mark();
+    spans.push_back({stage, a, b});
+  }
+  void finish(rnmf_stage_times& out) {
+    stop = mark();
+    RNMF_CUDA(cudaEventSynchronize(stop));
+    double acc[kNumStages] = {};
+    int64_t counts[kNumStages] = {};
+    for (auto& s : spans) {
+      float ms = 0.f;
+      RNMF_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
+      acc[s.stage] += ms;
+      counts[s.stage] += 1;
+    }
+    float tot = 0.f;
+    RNMF_CUDA(cudaEventElapsedTime(&tot, start, stop));
+    out.scan_ms = acc[kScan];
+    out.sketch_ms = acc[kSketch];
+    out.qr_ms = acc[kQr];
+    out.init_ms = acc[kInit];
+    out.sweeps_ms = acc[kSweeps];
+    out.metrics_ms = acc[kMetrics];
+    out.h2d_ms = acc[kH2D];
+    out.d2h_ms = acc[kD2H];
+    out.xw_ms = acc[kXw];
+    out.xtw_ms = acc[kXtw];
+    out.xw_launches = counts[kXw];
+    out.xtw_launches = counts[kXtw];
+    out.total_ms = tot;
+    out.kernel_launches = launches;
+  }
+};
+
+// ---- small host helpers -----------------------------------------------------------------------
+static void check_device_ptr(const rnmf_gpu_context* ctx, const void* p, const char* what) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess || attr.type != cudaMemoryTypeDevice ||
+      attr.device != ctx->device) {
+    cudaGetLastError();
+    throw ParameterError(std::string(what) + ": expected device memory of GPU " + std::to_string(ctx->device));
+  }
+}
+
+static void validate_options_after_data(int64_t m, int64_t n, const rnmf_solver_options& o) {
+  // p/src/hals.cpp:36-53 (check_nonnegative_finite already done by the scan)
+  const int64_t bound = std::min(m, n);
+  if (o.rank < 1 || o.rank > bound)
+    throw ParameterError("rank " + std::to_string(o.rank) + " out of range [1, " + std::to_string(bound) +
+                         "] for a " + shape_string(m, n) + " input");
+  if (o.max_iter < 0) throw ParameterError("max_iter must be nonnegative");
+  if (!(o.tol > 0.0)) throw ParameterError("tol must be positive");
+  if (o.reg.alpha_w < 0.0 || o.reg.alpha_h < 0.0 || o.reg.beta_w < 0.0 || o.reg.beta_h < 0.0)
+    throw ParameterError("regularization strengths must be nonnegative");
+  if (o.trace_full_every < 1) throw ParameterError("trace_full_every must be at least 1");
+  if (o.oversampling < 0 || o.power_iterations < 0)
+    throw ParameterError("oversampling and power iterations must be nonnegative");
+}
+
+static void check_supported(const rnmf_solver_options& o) {
+  if (o.init != RNMF_INIT_RANDOM)
+    throw ParameterError("B200 path: InitScheme::Svd is not implemented yet (use Random or pass w0/h0)");
+  if (o.order != RNMF_ORDER_GROUPED)
+    throw ParameterError("B200 path: only UpdateOrder::Grouped is implemented");
+  if (o.reseed_dead) throw ParameterError("B200 path: reseed_dead is not implemented");
+  if (o.math_mode != RNMF_MATH_EXACT && o.math_mode != RNMF_MATH_TF32X3 && o.math_mode != RNMF_MATH_TF32)
+    throw ParameterError("math_mode must be RNMF_MATH_EXACT, RNMF_MATH_TF32X3 or RNMF_MATH_TF32");
+}
+
+// sketch_width, p/src/sketch.cpp:30-50 (block_size is fixed at its default of 1024)
+static int64_t sketch_width(int64_t rows, int64_t cols, int64_t target_rank, int64_t oversampling,
+                            int64_t power_iterations) {
+  const int64_t bound = std::min(rows, cols);
+  if (target_rank < 1 || target_rank > bound)
+    throw ParameterError("sketch: target rank " + std::to_string(target_rank) + " out of range [1, " +
+                         std::to_string(bound) + "] for a " + shape_string(rows, cols) + " matrix");
+  if (oversampling < 0 || power_iterations < 0)
+    throw ParameterError("sketch: oversampling and power iterations must be nonnegative");
+  int64_t l = target_rank + oversampling;
+  if (l > bound) {
+    std::fprintf(stderr, "rnmf: sketch width %lld exceeds min(%lld, %lld); clamping to %lld\n", (long long)l,
+                 (long long)rows, (long long)cols, (long long)bound);
+    l = bound;
+  }
+  return l;
+}
+
+static void check_problem_shapes(const rnmf_problem_shape& s, const char* who) {  // p/src/rhals.cpp:11-21
+  const bool ok = s.q_rows == s.w_rows && s.q_cols == s.b_rows && s.wt_rows == s.q_cols &&
+                  s.wt_cols == s.w_cols && s.h_rows == s.w_cols && s.h_cols == s.b_cols;
+  if (!ok)
+    throw ShapeError(std::string(who) + ": inconsistent compressed problem, Q=" + shape_string(s.q_rows, s.q_cols) +
+                     ", B=" + shape_string(s.b_rows, s.b_cols) + ", W~=" + shape_string(s.wt_rows, s.wt_cols) +
+                     ", W=" + shape_string(s.w_rows, s.w_cols) + ", H=" + shape_string(s.h_rows, s.h_cols));
+}
+
+// ==============================================================================================
+template <typename T>
+class Engine {
+ public:
+  Engine(rnmf_gpu_context* ctx, Timer& tm) : ctx_(ctx), st_(ctx->stream), tm_(tm) {}
+
+  // Copy a caller matrix (host or device) into a context buffer.
+  T* import(const std::string& name, const void* src, int location, size_t count) {
+    T* dst = ctx_->d<T>(name, count);
+    if (count == 0) return dst;
+    if (location == RNMF_DEVICE) {
+      check_device_ptr(ctx_, src, name.c_str());
+      RNMF_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToDevice, st_));
+    } else {
+      tm_.span(kH2D, [&] { RNMF_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st_)); });
+    }
+    return dst;
+  }
+  void export_(void* dst, int location, const T* src, size_t count) {
+    if (count == 0 || dst == nullptr) return;
+    if (location == RNMF_DEVICE) {
+      check_device_ptr(ctx_, dst, "output");
+      RNMF_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToDevice, st_));
+    } else {
+      tm_.span(kD2H, [&] { RNMF_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, st_)); });
+    }
+  }
+  // Upload host doubles converted to T (small matrices: Omega, compressed-problem inputs).
+  T* upload_converted(const std::string& name, const double* src, size_t count) {
+    T* hst = ctx_->h<T>(name + ".pin", count);
+    for (size_t i = 0; i < count; ++i) hst[i] = T(src[i]);
+    T* dst = ctx_->d<T>(name, count);
+    tm_.span(kH2D, [&] { RNMF_CUDA(cudaMemcpyAsync(dst, hst, count * sizeof(T), cudaMemcpyHostToDevice, st_)); });
+    return dst;
+  }
+
+  // One pass over X: data checks + sum + sum of squares.  Throws DataError like
+  // check_nonnegative_finite (p/src/hals.cpp:17-34), non-finite before negative.
+  void scan(const T* x, int64_t m, int64_t n, bool check_negative, const char* nonfinite_msg) {
+    auto* bad = ctx_->d<unsigned long long>("scan.bad", 2);
+    auto* part = ctx_->d<double>("scan.part", 2 * scan_grid());
+    auto* out = ctx_->d<double>("scan.out", 2);
+    tm_.span(kScan, [&] { tm_.launches += launch_scan<T>(x, m * n, bad, part, out, st_); });
+    auto* hb = ctx_->h<unsigned long long>("scan.bad.h", 2);
+    auto* ho = ctx_->h<double>("scan.out.h", 2);
+    RNMF_CUDA(cudaMemcpyAsync(hb, bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+    RNMF_CUDA(cudaMemcpyAsync(ho, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    RNMF_CUDA(cudaStreamSynchronize(st_));
+    if (hb[0] != ~0ull) {
+      if (nonfinite_msg) throw DataError(nonfinite_msg);
+      const int64_t i = int64_t(hb[0]) / n, j = int64_t(hb[0]) % n;
+      throw DataError("input contains non-finite entries at (" + std::to_string(i) + "," + std::to_string(j) + ")");
+    }
+    if (check_negative && hb[1] != ~0ull) {
+      const int64_t i = int64_t(hb[1]) / n, j = int64_t(hb[1]) % n;
+      throw DataError("input contains negative entries at (" + std::to_string(i) + "," + std::to_string(j) + ")");
+    }
+    sum_ = ho[0];
+    sumsq_ = ho[1];
+  }
+
+  // rqb, p/src/sketch.cpp:52-71 -> Q (m x l), B (l x n) in context buffers.
+  void rqb(const T* x, int64_t m, int64_t n, int l, int64_t q_iters, const T* omega_dev, T** q_out, T** b_out) {
+    T* y = ctx_->d<T>("rqb.y", size_t(m) * l);
+    T* qb = ctx_->d<T>("rqb.q", size_t(m) * l);
+    T* p = ctx_->d<T>("rqb.p", size_t(n) * l);
+    T* z = ctx_->d<T>("rqb.z", size_t(n) * l);
+    T* b = ctx_->d<T>("rqb.b", size_t(l) * n);
+    const int splits = xtw_default_splits(m, n);
+    T* part = ctx_->d<T>("rqb.part", size_t(splits) * n * l);
+    const int64_t ws_len = std::max(tsqr_workspace_doubles(m, l, ctx_->max_smem), tsqr_workspace_doubles(n, l, ctx_->max_smem));
+    double* ws = ctx_->d<double>("tsqr.ws", size_t(ws_len));
+    const double xbytes = double(m) * double(n) * sizeof(T);
+    auto xw = [&](const T* s, T* out) {
+      tm_.span(kXw, [&] { tm_.launches += launch_xw<T>(x, m, n, s, l, out, st_); });
+      sketch_bytes_ += xbytes;
+      ctx_->last.xw_bytes += xbytes;
+      sketch_passes_ += 1;
+    };
+    auto xtw = [&](const T* s, T* out, bool tr) {
+      tm_.span(kXtw, [&] { tm_.launches += launch_xtw<T>(x, m, n, s, l, part, splits, out, tr, st_); });
+      sketch_bytes_ += xbytes;
+      ctx_->last.xtw_bytes += xbytes;
+      sketch_passes_ += 1;
+    };
+    auto qr = [&](const T* a, int64_t rows, T* out) {
+      tm_.span(kQr, [&] { tm_.launches += launch_tsqr<T>(a, rows, l, out, ws, ctx_->max_smem, st_); });
+    };
+    xw(omega_dev, y);
+    for (int64_t it = 0; it < q_iters; ++it) {
+      qr(y, m, qb);
+      xtw(qb, p, false);
+      qr(p, n, z);
+      xw(z, y);
+    }
+    qr(y, m, qb);
+    xtw(qb, b, true);
+    *q_out = qb;
+    *b_out = b;
+  }
+
+  // Full-space metrics (p/src/rhals.cpp:140-148) of the device factors w (m x k), h (k x n):
+  // writes [objective, pgrad_full] into res (device).
+  void metrics(const T* x, int64_t m, int64_t n, int k, const T* w, const T* h, double* res) {
+    T* ht = ctx_->d<T>("met.ht", size_t(n) * k);
+    double* hht = ctx_->d<double>("met.hht", size_t(k) * k);
+    double* wtw = ctx_->d<double>("met.wtw", size_t(k) * k);
+    double* gpart = ctx_->d<double>("met.gpart", size_t(gram_parts(std::max(m, n))) * k * k);
+    double* gpart2 = ctx_->d<double>("met.gpart2", size_t(gram_parts(std::max(m, n))) * k * k);
+    const int nb1 = xw_metrics_blocks(m);
+    double* pobj = ctx_->d<double>("met.pobj", size_t(nb1));
+    double* ppgw = ctx_->d<double>("met.ppgw", size_t(nb1));
+    const int splits = xtw_default_splits(m, n);
+    T* part = ctx_->d<T>("met.part", size_t(splits) * n * k);
+    double* ppgh = ctx_->d<double>("met.ppgh", size_t(ceil_div(n, 256)));
+    double* tmp = ctx_->d<double>("met.tmp", 4);
+    tm_.span(kMetrics, [&] {
+      tm_.launches += launch_transpose<T>(h, k, n, ht, st_);
+      tm_.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st_);
+      tm_.launches += launch_gram_rows<T>(w, m, k, gpart2, wtw, st_);
+      int b1 = 0, b2 = 0;
+      tm_.launches += launch_xw_metrics<T>(x, m, n, ht, w, k, hht, pobj, ppgw, &b1, st_);
+      tm_.launches += launch_xtw_metrics<T>(x, m, n, w, k, h, wtw, part, splits, ppgh, &b2, st_);
+      tm_.launches += launch_sum_parts(pobj, b1, res, st_);
+      tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
+      tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
+      // res[1] = pgw + pgh, done on device by a 2-element sum
+      tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
+    });
+    metrics_bytes_ += 2.0 * double(m) * double(n) * sizeof(T);
+    metrics_passes_ += 2;
+  }
+
+  double sum() const { return sum_; }
+  double sumsq() const { return sumsq_; }
+  double sketch_bytes_ = 0, metrics_bytes_ = 0;
+  int64_t sketch_passes_ = 0, metrics_passes_ = 0;
+
+ private:
+  rnmf_gpu_context* ctx_;
+  cudaStream_t st_;
+  Timer& tm_;
+  double sum_ = 0.0, sumsq_ = 0.0;
+};
+
+// ---- the sweep / trace loop shared by rhals_fit and rhals_fit_compressed ---------------------
+template <typename T>
+struct LoopIO {
+  const T* x;
+  int64_t m, n;
+  int l, k;
+  const T* q;
+  const T* b;
+  T* w;
+  T* h;
+  double* wt;  // device l x k (in/out)
+  bool init_wt;
+};
+
+template <typename T>
+static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnmf_solver_options& o, LoopIO<T>& io,
+                     std::chrono::steady_clock::time_point t0, double x_norm, rnmf_trace_record* trace,
+                     int64_t* trace_len) {
+  cudaStream_t st = ctx->stream;
+  const int l = io.l, k = io.k;
+  const int64_t max_iter = o.max_iter;
+  const SweepPlan plan = plan_sweeps<T>(io.m, io.n, l, k, ctx->sm_count, ctx->max_smem);
+  if (plan.grid == 0)
+    throw ParameterError("B200 path: problem " + shape_string(io.m, io.n) + " with l=" + std::to_string(l) +
+                         ", k=" + std::to_string(k) + " does not fit the persistent sweep kernel");
+  const int64_t plen = sweep_part_len(l, k);
+  SweepArgs<T> a{};
+  a.q = io.q;
+  a.b = io.b;
+  a.w = io.w;
+  a.h = io.h;
+  a.wt = io.wt;
+  a.wn = ctx->d<double>("sw.wn", size_t(k));
+  a.tm = ctx->d<double>("sw.tm", size_t(l) * k);
+  a.vm = ctx->d<double>("sw.vm", size_t(k) * k);
+  a.em = ctx->d<double>("sw.em", size_t(l) * k);
+  a.m = io.m;
+  a.n = io.n;
+  a.l = l;
+  a.k = k;
+  a.alpha_w = o.reg.alpha_w;
+  a.alpha_h = o.reg.alpha_h;
+  a.beta_w = o.reg.beta_w;
+  a.beta_h = o.reg.beta_h;
+  a.stop_rule = o.stopping;
+  a.tol = o.tol;
+  a.pgrad0 = ctx->d<double>("sw.pgrad0", 1);
+  a.trace_objc = ctx->d<double>("sw.tobjc", size_t(max_iter + 1));
+  a.trace_pgrad = ctx->d<double>("sw.tpgrad", size_t(max_iter + 1));
+  a.trace_time = ctx->d<unsigned long long>("sw.ttime", size_t(max_iter + 1));
+  a.status = ctx->d<long long>("sw.status", 2);
+  a.barrier = ctx->d<unsigned>("sw.barrier", 1);
+  a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
+  a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+
+  // Metrics results, one slot per evaluation: [objective, pgrad_full]
+  const int64_t max_evals = max_iter / o.trace_full_every + 4 + (o.stopping == RNMF_STOP_OBJECTIVE ? max_iter : 0);
+  double* mres = ctx->d<double>("sw.mres", size_t(2 * max_evals));
+  std::vector<int64_t> eval_iter;
+
+  // host <-> device clock reference for elapsed_s
+  auto* gt_ref = ctx->d<unsigned long long>("sw.gtref", 1);
+  RNMF_CUDA(cudaStreamSynchronize(st));
+  const double h_ref = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  tm.launches += launch_timestamp(gt_ref, st);
+
+  // record 0: full-space metrics of the initial factors
+  eng.metrics(io.x, io.m, io.n, k, io.w, io.h, mres);
+  eval_iter.push_back(0);
+
+  auto* hstat = ctx->h<long long>("sw.status.h", 2);
+  auto* hmres = ctx->h<double>("sw.mres.h", size_t(2 * max_evals));
+  const bool objective_rule = o.stopping == RNMF_STOP_OBJECTIVE;
+  const int64_t tfe = o.trace_full_every;
+  int64_t t_begin = 1;
+  bool first = true;
+  int64_t last = 0;
+  while (true) {
+    // chunks end at the next full-metrics point (p/src/rhals.cpp:191-193)
+    const int64_t t_end = std::min(max_iter, objective_rule ? t_begin : ceil_div(t_begin, tfe) * tfe);
+    a.flags = kRecord | kDoW | kDoH | (first ? (kEval0 | kInitWn | (io.init_wt ? kInitWt : 0)) : 0);
+    a.t_begin = t_begin;
+    a.t_end = t_end;
+    tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
+    RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaStreamSynchronize(st));
+    first = false;
+    last = hstat[0];
+    const bool stopped = hstat[1] != 0;
+    if (last >= t_begin) {
+      eng.metrics(io.x, io.m, io.n, k, io.w, io.h, mres + 2 * eval_iter.size());
+      eval_iter.push_back(last);
+    }
+    bool stop = stopped;
+    if (objective_rule && last >= t_begin) {
+      RNMF_CUDA(cudaMemcpyAsync(hmres, mres + 2 * (eval_iter.size() - 1), 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      RNMF_CUDA(cudaStreamSynchronize(st));
+      stop = hmres[0] < o.tol;  // p/src/rhals.cpp:198-199
+    }
+    if (stop || last >= max_iter || last < t_end) break;  // last < t_end: stationary start
+    t_begin = last + 1;
+  }
+  // gather the trace
+  const int64_t nrec = last + 1;
+  auto* hobjc = ctx->h<double>("sw.tobjc.h", size_t(nrec));
+  auto* hpg = ctx->h<double>("sw.tpgrad.h", size_t(nrec));
+  auto* htime = ctx->h<unsigned long long>("sw.ttime.h", size_t(nrec));
+  auto* hgt = ctx->h<unsigned long long>("sw.gtref.h", 1);
+  tm.span(kD2H, [&] {
+    RNMF_CUDA(cudaMemcpyAsync(hobjc, a.trace_objc, size_t(nrec) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaMemcpyAsync(hpg, a.trace_pgrad, size_t(nrec) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaMemcpyAsync(htime, a.trace_time, size_t(nrec) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaMemcpyAsync(hgt, gt_ref, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaMemcpyAsync(hmres, mres, 2 * eval_iter.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  });
+  RNMF_CUDA(cudaStreamSynchronize(st));
+  size_t ev = 0;
+  double obj = 0, rel = 0, pgf = 0;
+  for (int64_t t = 0; t < nrec; ++t) {
+    while (ev < eval_iter.size() && eval_iter[ev] <= t) {
+      obj = hmres[2 * ev];
+      pgf = hmres[2 * ev + 1];
+      rel = x_norm > 0.0 ? std::sqrt(obj) / x_norm : 0.0;
+      ++ev;
+    }
+    rnmf_trace_record& r = trace[t];
+    r.iter = t;
+    r.objective = obj;
+    r.rel_err = rel;
+    r.pgrad = hpg[t];
+    r.pgrad_full = pgf;
+    r.objective_compressed = hobjc[t];
+    const double dt = double((long long)(htime[t] - hgt[0])) * 1e-9;
+    r.elapsed_s = h_ref + std::max(0.0, dt);
+  }
+  for (int64_t t = 1; t < nrec; ++t) trace[t].elapsed_s = std::max(trace[t].elapsed_s, trace[t - 1].elapsed_s);
+  *trace_len = nrec;
+  ctx->last.sweeps = last;
+}
+
+// ---- random draws for Omega / init (reference streams unless overridden) ---------------------
+static void fill_uniform(Rng& rng, double* out, size_t count) {
+  for (size_t i = 0; i < count; ++i) out[i] = rng.uniform();
+}
+static void fill_gaussian(Rng& rng, double* out, size_t count) {
+  for (size_t i = 0; i < count; ++i) out[i] = rng.gaussian();
+}
+
+template <typename T>
+static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int64_t m, int64_t n,
+                     const rnmf_solver_options& o, const double* omega, const double* w0, const double* h0,
+                     void* w_out, void* h_out, rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len,
+                     void* q_out, void* b_out, void* wt_out, int64_t* l_out, bool fit) {
+  const auto t0 = std::chrono::steady_clock::now();
+  ctx->last = rnmf_stage_times{};
+  Timer tm(ctx);
+  Engine<T> eng(ctx, tm);
+  if (m < 0 || n < 0) throw ShapeError("X has negative dimensions " + shape_string(m, n));
+  const T* x = nullptr;
+  if (m * n > 0) {
+    x = eng.import("x", x_in, location, size_t(m) * n);
+    eng.scan(x, m, n, true, nullptr);
+  }
+  validate_options_after_data(m, n, o);
+  check_supported(o);
+  if (fit && trace_cap < o.max_iter + 1)
+    throw ParameterError("trace buffer too small: need " + std::to_string(o.max_iter + 1) + " records, have " +
+                         std::to_string(trace_cap));
+  const int k = int(o.rank);
+  const int64_t l64 = sketch_width(m, n, o.rank, o.oversampling, o.power_iterations);
+  const int l = int(l64);
+  if (l > tsqr_max_l(ctx->max_smem) || l > 128)
+    throw ParameterError("B200 path: sketch width " + std::to_string(l) + " above the supported maximum " +
+                         std::to_string(std::min(128, tsqr_max_l(ctx->max_smem))));
+  if (k > 64) throw ParameterError("B200 path: rank above 64 is not supported yet");
+  if (l_out) *l_out = l;
+
+  // Omega: p/src/rhals.cpp:87-92 -> uniform from Rng(Rng(seed).split(3).seed())
+  std::vector<double> om_host;
+  const double* om = omega;
+  if (!om) {
+    om_host.resize(size_t(n) * l);
+    Rng rng(Rng(o.seed).split(kSketchStream).seed());
+    fill_uniform(rng, om_host.data(), om_host.size());
+    om = om_host.data();
+  }
+  T* om_dev = eng.upload_converted("omega", om, size_t(n) * l);
+
+  // initial draws on a host thread while the GPU sketches (random_init, p/src/hals.cpp:118-124)
+  double* uw = ctx->h<double>("init.uw", size_t(m) * k);
+  double* uh = ctx->h<double>("init.uh", size_t(k) * n);
+  std::thread drawer([&] {
+    if (w0 && h0) {
+      std::memcpy(uw, w0, sizeof(double) * size_t(m) * k);
+      std::memcpy(uh, h0, sizeof(double) * size_t(k) * n);
+      return;
+    }
+    Rng rng(o.seed);
+    if (w0)
+      std::memcpy(uw, w0, sizeof(double) * size_t(m) * k);
+    else
+      fill_uniform(rng, uw, size_t(m) * k);
+    if (h0)
+      std::memcpy(uh, h0, sizeof(double) * size_t(k) * n);
+    else
+      fill_uniform(rng, uh, size_t(k) * n);
+  });
+  T *q = nullptr, *b = nullptr;
+  try {
+    tm.span(kSketch, [&] { eng.rqb(x, m, n, l, o.power_iterations, om_dev, &q, &b); });
+  } catch (...) {
+    drawer.join();
+    throw;
+  }
+  drawer.join();
+
+  const double scale = std::sqrt(eng.sum() / double(m * n) / double(k));
+  T* w = ctx->d<T>("w", size_t(m) * k);
+  T* h = ctx->d<T>("h", size_t(k) * n);
+  double* uw_d = ctx->d<double>("init.uw.d", size_t(m) * k);
+  double* uh_d = ctx->d<double>("init.uh.d", size_t(k) * n);
+  tm.span(kH2D, [&] {
+    RNMF_CUDA(cudaMemcpyAsync(uw_d, uw, sizeof(double) * size_t(m) * k, cudaMemcpyHostToDevice, ctx->stream));
+    RNMF_CUDA(cudaMemcpyAsync(uh_d, uh, sizeof(double) * size_t(k) * n, cudaMemcpyHostToDevice, ctx->stream));
+  });
+  tm.span(kInit, [&] {
+    tm.launches += launch_scale_cast<T>(uw_d, int64_t(m) * k, scale, w, ctx->stream);
+    tm.launches += launch_scale_cast<T>(uh_d, int64_t(k) * n, scale, h, ctx->stream);
+  });
+  double* wt = ctx->d<double>("wt", size_t(l) * k);
+  const double x_norm = std::sqrt(eng.sumsq());
+
+  if (fit) {
+    LoopIO<T> io{x, m, n, l, k, q, b, w, h, wt, true};
+    rnmf_solver_options oo = o;
+    run_loop<T>(ctx, eng, tm, oo, io, t0, x_norm, trace, trace_len);
+    eng.export_(w_out, location, w, size_t(m) * k);
+    eng.export_(h_out, location, h, size_t(k) * n);
+  } else {
+    // compress: W~ = Q^T W via the sweep kernel's init phase (p/src/rhals.cpp:103)
+    const SweepPlan plan = plan_sweeps<T>(m, n, l, k, ctx->sm_count, ctx->max_smem);
+    if (plan.grid == 0) throw ParameterError("B200 path: problem does not fit the persistent sweep kernel");
+    SweepArgs<T> a{};
+    a.q = q;
+    a.b = b;
+    a.w = w;
+    a.h = h;
+    a.wt = wt;
+    a.wn = ctx->d<double>("sw.wn", size_t(k));
+    a.tm = ctx->d<double>("sw.tm", size_t(l) * k);
+    a.vm = ctx->d<double>("sw.vm", size_t(k) * k);
+    a.em = ctx->d<double>("sw.em", size_t(l) * k);
+    a.m = m, a.n = n, a.l = l, a.k = k;
+    a.flags = kInitWt | kInitWn;
+    a.t_begin = 1, a.t_end = 0;
+    a.pgrad0 = ctx->d<double>("sw.pgrad0", 1);
+    a.trace_objc = ctx->d<double>("sw.tobjc", 1);
+    a.trace_pgrad = ctx->d<double>("sw.tpgrad", 1);
+    a.trace_time = ctx->d<unsigned long long>("sw.ttime", 1);
+    a.status = ctx->d<long long>("sw.status", 2);
+    a.barrier = ctx->d<unsigned>("sw.barrier", 1);
+    const int64_t plen = sweep_part_len(l, k);
+    a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
+    a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+    tm.span(kInit, [&] { tm.launches += launch_sweeps<T>(a, plan, ctx->stream); });
+    eng.export_(q_out, location, q, size_t(m) * l);
+    eng.export_(b_out, location, b, size_t(l) * n);
+    if (wt_out) {
+      T* wt_t = ctx->d<T>("wt.cast", size_t(l) * k);
+      // device-side cast of W~ to the call's dtype
+      tm.launches += launch_scale_cast<T>(wt, int64_t(l) * k, 1.0, wt_t, ctx->stream);
+      eng.export_(wt_out, location, wt_t, size_t(l) * k);
+    }
+    eng.export_(w_out, location, w, size_t(m) * k);
+    eng.export_(h_out, location, h, size_t(k) * n);
+  }
+  ctx->last.sketch_bytes = eng.sketch_bytes_;
+  ctx->last.metrics_bytes = eng.metrics_bytes_;
+  ctx->last.sketch_passes = eng.sketch_passes_;
+  ctx->last.metrics_passes = eng.metrics_passes_;
+  const double xwb = ctx->last.xw_bytes, xtwb = ctx->last.xtw_bytes;
+  const int64_t sweeps = ctx->last.sweeps;
+  tm.finish(ctx->last);
+  ctx->last.xw_bytes = xwb;
+  ctx->last.xtw_bytes = xtwb;
+  ctx->last.sweeps = sweeps;
+  ctx->last.sketch_bytes = eng.sketch_bytes_;
+  ctx->last.metrics_bytes = eng.metrics_bytes_;
+  ctx->last.sketch_passes = eng.sketch_passes_;
+  ctx->last.metrics_passes = eng.metrics_passes_;
+}
+
+template <typename T>
+static void rqb_impl(rnmf_gpu_context* ctx, const void* a_in, int location, int64_t m, int64_t n, int64_t rank,
+                     int64_t p, int64_t qi, int test_matrix, uint64_t seed, const double* omega, void* q_out,
+                     void* b_out, int64_t* l_out) {
+  ctx->last = rnmf_stage_times{};
+  Timer tm(ctx);
+  Engine<T> eng(ctx, tm);
+  const int64_t l64 = sketch_width(m, n, rank, p, qi);  // ParameterError before the data check
+  if (l_out) *l_out = l64;
+  if (!q_out && !b_out) {
+    tm.finish(ctx->last);
+    return;
+  }
+  const int l = int(l64);
+  if (l > tsqr_max_l(ctx->max_smem) || l > 128)
+    throw ParameterError("B200 path: sketch width " + std::to_string(l) + " above the supported maximum");
+  const T* x = eng.import("x", a_in, location, size_t(m) * n);
+  eng.scan(x, m, n, false, "rqb: input contains non-finite values");  // p/src/sketch.cpp:54-56
+  std::vector<double> om_host;
+  const double* om = omega;
+  if (!om) {
+    om_host.resize(size_t(n) * l);
+    Rng rng(seed);
+    if (test_matrix == RNMF_TEST_UNIFORM)
+      fill_uniform(rng, om_host.data(), om_host.size());
+    else
+      fill_gaussian(rng, om_host.data(), om_host.size());
+    om = om_host.data();
+  }
+  T* om_dev = eng.upload_converted("omega", om, size_t(n) * l);
+  T *q = nullptr, *b = nullptr;
+  tm.span(kSketch, [&] { eng.rqb(x, m, n, l, qi, om_dev, &q, &b); });
+  eng.export_(q_out, location, q, size_t(m) * l);
+  eng.export_(b_out, location, b, size_t(l) * n);
+  const double xwb = ctx->last.xw_bytes, xtwb = ctx->last.xtw_bytes;
+  tm.finish(ctx->last);
+  ctx->last.xw_bytes = xwb;
+  ctx->last.xtw_bytes = xtwb;
+  ctx->last.sketch_bytes = eng.sketch_bytes_;
+  ctx->last.sketch_passes = eng.sketch_passes_;
+}
+
+// Stage API: rhals_update_W / rhals_update_H on a caller-supplied compressed problem, and the
+// fit loop started from one.
+template <typename T>
+static void stage_impl(rnmf_gpu_context* ctx, int location, const rnmf_problem_shape& s, const void* q_in,
+                       const void* b_in, void* wt_io, void* w_io, void* h_io, const rnmf_reg_config& reg, bool do_w,
+                       const char* who) {
+  ctx->last = rnmf_stage_times{};
+  check_problem_shapes(s, who);
+  Timer tm(ctx);
+  Engine<T> eng(ctx, tm);
+  const int64_t m = s.q_rows, n = s.b_cols;
+  const int l = int(s.q_cols), k = int(s.w_cols);
+  if (m == 0 || n == 0 || l == 0 || k == 0) {
+    tm.finish(ctx->last);
+    return;
+  }
+  if (l > 128 || k > 64) throw ParameterError("B200 path: l <= 128 and k <= 64 supported");
+  const T* q = eng.import("st.q", q_in, location, size_t(m) * l);
+  const T* b = eng.import("st.b", b_in, location, size_t(l) * n);
+  T* wt_t = eng.import("st.wt", wt_io, location, size_t(l) * k);
+  T* w = eng.import("st.w", w_io, location, size_t(m) * k);
+  T* h = eng.import("st.h", h_io, location, size_t(k) * n);
+  double* wt = ctx->d<double>("st.wt.d", size_t(l) * k);
+  tm.launches += launch_widen<T>(wt_t, int64_t(l) * k, wt, ctx->stream);
+  const SweepPlan plan = plan_sweeps<T>(m, n, l, k, ctx->sm_count, ctx->max_smem);
+  if (plan.grid == 0) throw ParameterError("B200 path: problem does not fit the persistent sweep kernel");
+  SweepArgs<T> a{};
+  a.q = q, a.b = b, a.w = w, a.h = h, a.wt = wt;
+  a.wn = ctx->d<double>("sw.wn", size_t(k));
+  a.tm = ctx->d<double>("sw.tm", size_t(l) * k);
+  a.vm = ctx->d<double>("sw.vm", size_t(k) * k);
+  a.em = ctx->d<double>("sw.em", size_t(l) * k);
+  a.m = m, a.n = n, a.l = l, a.k = k;
+  a.alpha_w = reg.alpha_w, a.alpha_h = reg.alpha_h, a.beta_w = reg.beta_w, a.beta_h = reg.beta_h;
+  a.flags = do_w ? (kTvOnly | kDoW) : (kInitWn | kDoH);
+  a.t_begin = 1, a.t_end = 1;
+  a.pgrad0 = ctx->d<double>("sw.pgrad0", 1);
+  a.trace_objc = ctx->d<double>("sw.tobjc", 2);
+  a.trace_pgrad = ctx->d<double>("sw.tpgrad", 2);
+  a.trace_time = ctx->d<unsigned long long>("sw.ttime", 2);
+  a.status = ctx->d<long long>("sw.status", 2);
+  a.barrier = ctx->d<unsigned>("sw.barrier", 1);
+  const int64_t plen = sweep_part_len(l, k);
+  a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
+  a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+  tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, ctx->stream); });
+  if (do_w) {
+    T* wt_cast = ctx->d<T>("st.wt.cast", size_t(l) * k);
+    tm.launches += launch_scale_cast<T>(wt, int64_t(l) * k, 1.0, wt_cast, ctx->stream);
+    eng.export_(wt_io, location, wt_cast, size_t(l) * k);
+    eng.export_(w_io, location, w, size_t(m) * k);
+  } else {
+    eng.export_(h_io, location, h, size_t(k) * n);
+  }
+  tm.finish(ctx->last);
+}
+
+template <typename T>
+static void fit_compressed_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int64_t m, int64_t n,
+                                const rnmf_solver_options& o, const rnmf_problem_shape& s, const void* q_in,
+                                const void* b_in, void* wt_io, void* w_io, void* h_io, rnmf_trace_record* trace,
+                                int64_t trace_cap, int64_t* trace_len) {
+  const auto t0 = std::chrono::steady_clock::now();
+  ctx->last = rnmf_stage_times{};
+  Timer tm(ctx);
+  Engine<T> eng(ctx, tm);
+  const T* x = nullptr;
+  if (m * n > 0) {
+    x = eng.import("x", x_in, location, size_t(m) * n);
+    eng.scan(x, m, n, true, nullptr);
+  }
+  validate_options_after_data(m, n, o);
+  check_supported(o);
+  check_problem_shapes(s, "rhals_fit_compressed");
+  if (s.q_rows != m || s.b_cols != n || s.w_cols != o.rank)
+    throw ShapeError("rhals_fit_compressed: problem does not match X=" + shape_string(m, n));
+  if (trace_cap < o.max_iter + 1)
+    throw ParameterError("trace buffer too small: need " + std::to_string(o.max_iter + 1) + " records, have " +
+                         std::to_string(trace_cap));
+  const int l = int(s.q_cols), k = int(s.w_cols);
+  if (l > 128 || k > 64) throw ParameterError("B200 path: l <= 128 and k <= 64 supported");
+  const T* q = eng.import("st.q", q_in, location, size_t(m) * l);
+  const T* b = eng.import("st.b", b_in, location, size_t(l) * n);
+  T* wt_t = eng.import("st.wt", wt_io, location, size_t(l) * k);
+  T* w = eng.import("w", w_io, location, size_t(m) * k);
+  T* h = eng.import("h", h_io, location, size_t(k) * n);
+  double* wt = ctx->d<double>("wt", size_t(l) * k);
+  tm.launches += launch_widen<T>(wt_t, int64_t(l) * k, wt, ctx->stream);
+  LoopIO<T> io{x, m, n, l, k, q, b, w, h, wt, false};
+  run_loop<T>(ctx, eng, tm, o, io, t0, std::sqrt(eng.sumsq()), trace, trace_len);
+  T* wt_cast = ctx->d<T>("st.wt.cast", size_t(l) * k);
+  tm.launches += launch_scale_cast<T>(wt, int64_t(l) * k, 1.0, wt_cast, ctx->stream);
+  eng.export_(wt_io, location, wt_cast, size_t(l) * k);
+  eng.export_(w_io, location, w, size_t(m) * k);
+  eng.export_(h_io, location, h, size_t(k) * n);
+  const int64_t sweeps = ctx->last.sweeps;
+  tm.finish(ctx->last);
+  ctx->last.sweeps = sweeps;
+  ctx->last.metrics_bytes = eng.metrics_bytes_;
+  ctx->last.metrics_passes = eng.metrics_passes_;
+}
+
+}  // namespace rnmf_gpu
+
+// =================================================================================================
+// C ABI
+namespace {
+
+void put_err(char* err, size_t cap, const std::string& msg) {
+  if (err && cap) {
+    const size_t n = std::min(cap - 1, msg.size());
+    std::memcpy(err, msg.data(), n);
+    err[n] = '\0';
+  }
+}
+
+template <typename F>
+int guarded(char* err, size_t cap, F&& f) {
+  try {
+    f();
+    put_err(err, cap, "");
+    return RNMF_OK;
+  } catch (const rnmf_gpu::ShapeError& e) {
+    put_err(err, cap, e.what());
+    return RNMF_SHAPE_ERROR;
+  } catch (const rnmf_gpu::ParameterError& e) {
+    put_err(err, cap, e.what());
+    return RNMF_PARAMETER_ERROR;
+  } catch (const rnmf_gpu::DataError& e) {
+    put_err(err, cap, e.what());
+    return RNMF_DATA_ERROR;
+  } catch (const std::exception& e) {
+    put_err(err, cap, e.what());
+    return RNMF_CUDA_ERROR;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    RNMF_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void check_ctx(const rnmf_gpu_context* ctx) {
+  if (!ctx) throw rnmf_gpu::ParameterError("null rnmf_gpu_context");
+}
+void check_dtype(int dtype, int location) {
+  if (dtype != RNMF_F32 && dtype != RNMF_F64) throw rnmf_gpu::ParameterError("dtype must be RNMF_F32 or RNMF_F64");
+  if (location != RNMF_HOST && location != RNMF_DEVICE)
+    throw rnmf_gpu::ParameterError("location must be RNMF_HOST or RNMF_DEVICE");
+}
+
+}  // namespace
+
+extern "C" {
+
+int rnmf_version(char* buf, size_t cap) {
+  put_err(buf, cap, "rnmf-b200 0.1.0 (sm_100a; reference rnmf 0.1.0, p/include/rnmf/version.hpp:7)");
+  return RNMF_OK;
+}
+
+void rnmf_default_options(rnmf_solver_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->rank = 0;
+  o->max_iter = 200;
+  o->tol = 1e-4;
+  o->init = RNMF_INIT_RANDOM;
+  o->order = RNMF_ORDER_GROUPED;
+  o->stopping = RNMF_STOP_PROJECTED_GRADIENT;
+  o->reseed_dead = 0;
+  o->seed = 0;
+  o->trace_full_every = 10;
+  o->oversampling = 20;
+  o->power_iterations = 2;
+  o->math_mode = RNMF_MATH_EXACT;
+}
+
+int rnmf_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int rnmf_gpu_context_create(int device, rnmf_gpu_context** out, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    if (!out) throw rnmf_gpu::ParameterError("null output pointer");
+    *out = nullptr;
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      throw rnmf_gpu::CudaError(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                "); the B200 path has no CPU fallback");
+    }
+    if (device < 0 || device >= count)
+      throw rnmf_gpu::ParameterError("device " + std::to_string(device) + " out of range [0, " +
+                                     std::to_string(count) + ")");
+    DeviceGuard g(device);
+    cudaDeviceProp prop{};
+    RNMF_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw rnmf_gpu::CudaError("device " + std::to_string(device) + " (" + prop.name +
+                                ") is not a Blackwell sm_100 part; this library is built for sm_100a only");
+    auto ctx = std::make_unique<rnmf_gpu_context>();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    ctx->max_smem = int(prop.sharedMemPerBlockOptin);
+    RNMF_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    *out = ctx.release();
+  });
+}
+
+void rnmf_gpu_context_destroy(rnmf_gpu_context* ctx) {
+  if (!ctx) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->dev)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& kv : ctx->pinned)
+    if (kv.second.p) cudaFreeHost(kv.second.p);
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete ctx;
+}
+
+int rnmf_gpu_last_stage_times(const rnmf_gpu_context* ctx, rnmf_stage_times* out) {
+  if (!ctx || !out) return RNMF_PARAMETER_ERROR;
+  *out = ctx->last;
+  return RNMF_OK;
+}
+
+int rnmf_gpu_rhals_fit(rnmf_gpu_context* ctx, const void* x, int dtype, int location, int64_t m, int64_t n,
+                       const rnmf_solver_options* opts, const double* omega, const double* w0, const double* h0,
+                       void* w_out, void* h_out, rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len,
+                       char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!opts || !trace || !trace_len) throw rnmf_gpu::ParameterError("null options / trace pointer");
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      fit_impl<float>(ctx, x, location, m, n, *opts, omega, w0, h0, w_out, h_out, trace, trace_cap, trace_len,
+                      nullptr, nullptr, nullptr, nullptr, true);
+    else
+      fit_impl<double>(ctx, x, location, m, n, *opts, omega, w0, h0, w_out, h_out, trace, trace_cap, trace_len,
+                       nullptr, nullptr, nullptr, nullptr, true);
+  });
+}
+
+int rnmf_gpu_rhals_fit_compressed(rnmf_gpu_context* ctx, const void* x, int dtype, int location, int64_t m,
+                                  int64_t n, const rnmf_solver_options* opts, const rnmf_problem_shape* shape,
+                                  const void* q, const void* b, void* wt, void* w, void* h, rnmf_trace_record* trace,
+                                  int64_t trace_cap, int64_t* trace_len, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!opts || !shape || !trace || !trace_len) throw rnmf_gpu::ParameterError("null argument");
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      fit_compressed_impl<float>(ctx, x, location, m, n, *opts, *shape, q, b, wt, w, h, trace, trace_cap, trace_len);
+    else
+      fit_compressed_impl<double>(ctx, x, location, m, n, *opts, *shape, q, b, wt, w, h, trace, trace_cap, trace_len);
+  });
+}
+
+int rnmf_gpu_compress(rnmf_gpu_context* ctx, const void* x, int dtype, int location, int64_t m, int64_t n,
+                      const rnmf_solver_options* opts, const double* omega, const double* w0, const double* h0,
+                      void* q_out, void* b_out, void* wt_out, void* w_out, void* h_out, int64_t* l_out, char* err,
+                      size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!opts) throw rnmf_gpu::ParameterError("null options");
+    DeviceGuard g(ctx->device);
+    int64_t dummy_len = 0;
+    if (dtype == RNMF_F32)
+      fit_impl<float>(ctx, x, location, m, n, *opts, omega, w0, h0, w_out, h_out, nullptr, 0, &dummy_len, q_out,
+                      b_out, wt_out, l_out, false);
+    else
+      fit_impl<double>(ctx, x, location, m, n, *opts, omega, w0, h0, w_out, h_out, nullptr, 0, &dummy_len, q_out,
+                       b_out, wt_out, l_out, false);
+  });
+}
+
+int rnmf_gpu_rqb(rnmf_gpu_context* ctx, const void* a, int dtype, int location, int64_t m, int64_t n,
+                 int64_t target_rank, int64_t oversampling, int64_t power_iterations, int test_matrix, uint64_t seed,
+                 const double* omega, int math_mode, void* q_out, void* b_out, int64_t* l_out, char* err,
+                 size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    (void)math_mode;
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      rqb_impl<float>(ctx, a, location, m, n, target_rank, oversampling, power_iterations, test_matrix, seed, omega,
+                      q_out, b_out, l_out);
+    else
+      rqb_impl<double>(ctx, a, location, m, n, target_rank, oversampling, power_iterations, test_matrix, seed, omega,
+                       q_out, b_out, l_out);
+  });
+}
+
+int rnmf_gpu_rhals_update_W(rnmf_gpu_context* ctx, int dtype, int location, const rnmf_problem_shape* shape,
+                            const void* q, const void* b, void* wt, void* w, const void* h, const rnmf_reg_config* reg,
+                            char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!shape || !reg) throw rnmf_gpu::ParameterError("null argument");
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      stage_impl<float>(ctx, location, *shape, q, b, wt, w, const_cast<void*>(h), *reg, true, "rhals_update_W");
+    else
+      stage_impl<double>(ctx, location, *shape, q, b, wt, w, const_cast<void*>(h), *reg, true, "rhals_update_W");
+  });
+}
+
+int rnmf_gpu_rhals_update_H(rnmf_gpu_context* ctx, int dtype, int location, const rnmf_problem_shape* shape,
+                            const void* q, const void* b, const void* wt, const void* w, void* h,
+                            const rnmf_reg_config* reg, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!shape || !reg) throw rnmf_gpu::ParameterError("null argument");
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      stage_impl<float>(ctx, location, *shape, q, b, const_cast<void*>(wt), const_cast<void*>(w), h, *reg, false,
+                        "rhals_update_H");
+    else
+      stage_impl<double>(ctx, location, *shape, q, b, const_cast<void*>(wt), const_cast<void*>(w), h, *reg, false,
+                         "rhals_update_H");
+  });
+}
+
+}  // extern "C"
