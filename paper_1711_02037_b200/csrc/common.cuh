@@ -71,12 +71,12 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch)
   __syncthreads();
   epoch += 1;
   if (threadIdx.x == 0) {
+    // bar.sync orders the CTA's writes before this release (cumulativity); the acquire load
+    // orders every later read of the CTA (after the bar.sync below) after all arrivals.
     const unsigned target = epoch * gridDim.x;
-    __threadfence();
     red_release_gpu_add(counter, 1u);
     while (ld_acquire_gpu(counter) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }

@@ -36,12 +36,24 @@ constexpr int kSwThreads = 256;
 constexpr int kSwWarps = kSwThreads / 32;
 constexpr int kMaxPerLane = 4;  // k, l <= 128
 constexpr double kDivisionFloor = 1e-12;  // p/include/rnmf/hals.hpp:67
+constexpr int kMaxGrid = 256;
+constexpr int kMaxLSlots = 5;     // (l + 1) / 32 lane slots in the recompress reduction
+constexpr int kMaxResSlots = 8;   // l / 16 lane slots for residc
+constexpr int kRedStride = 132;   // >= l + 1
+constexpr int kRedLen = kSwWarps * kRedStride > kSwThreads ? kSwWarps * kRedStride : kSwThreads;
+constexpr int kMaxGridPerLane = kMaxGrid / 32;
+
+// profile buckets (cycles of CTA 0, thread 0)
+enum {
+  kPfWStep, kPfLift, kPfRecomp, kPfBarrier1, kPfReduce1, kPfHCols, kPfHProducts, kPfBarrier2, kPfReduce2a,
+  kPfReduce2b, kPfPgw, kPfOther, kPfSweeps, kPfCount
+};
 
 struct SmemLayout {
   // fp64 region
-  size_t wt, tm, em, vm, sm, wn, red, scal, doubles_end;
+  size_t wt, tm, em, vm, sm, wn, pm, colold, colnew, invd, red, scal, doubles_end;
   // T region (offsets in bytes from the start)
-  size_t qs, wst, wcol, bc, hc, rc, total;
+  size_t qs, wst, wcold, bc, hc, rc, total;
 };
 
 template <typename T>
@@ -53,13 +65,17 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
     d += count;
     return off;
   };
-  L.wt = take(size_t(l) * k);
-  L.tm = take(size_t(l) * k);
-  L.em = take(size_t(l) * k);
+  L.wt = take(size_t(l) * (k + 1));
+  L.tm = take(size_t(l) * (k + 1));
+  L.em = take(size_t(l) * (k + 1));
   L.vm = take(size_t(k) * k);
   L.sm = take(size_t(k) * k);
   L.wn = take(size_t(k));
-  L.red = take(kSwThreads + 2 * kSwWarps);
+  L.pm = take(size_t(l) * (k + 1));
+  L.colold = take(size_t(l));
+  L.colnew = take(size_t(l));
+  L.invd = take(size_t(k));
+  L.red = take(kRedLen + 2 * kSwWarps);
   L.scal = take(16);
   L.doubles_end = d * sizeof(double);
   size_t b = (L.doubles_end + 15) / 16 * 16;
@@ -69,9 +85,14 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
     return off;
   };
   const size_t ncp = size_t(NCM) + 1;
-  L.qs = qs ? takeT(size_t(RM) * (l + 1)) : 0;
+  auto takeD = [&](size_t count) {
+    const size_t off = b;
+    b += (count * sizeof(double) + 15) / 16 * 16;
+    return off;
+  };
+  L.qs = qs ? takeD(size_t(RM) * (l + 1)) : 0;
+  L.wcold = takeD(size_t(RM));
   L.wst = qs ? takeT(size_t(k) * RM) : 0;
-  L.wcol = qs ? 0 : takeT(size_t(RM));
   L.bc = takeT(size_t(l) * ncp);
   L.hc = takeT(size_t(k) * ncp);
   L.rc = takeT(size_t(l) * ncp);
@@ -84,11 +105,23 @@ struct Sweeper {
   const SweepArgs<T>& a;
   int G, g, tid, lane, wid, l, k;
   int64_t r0, R, c0, NC, RM;
-  int ncp, lq;
-  double *Wt, *Tm, *Em, *Vm, *Sm, *wn, *red, *scal;
-  T *Qs, *WsT, *wcol, *Bc, *Hc, *Rc;
+  int ncp, lq, kp;  // kp = k + 1: odd fp64 row stride of the l x k arrays (bank-conflict free columns)
+  double *Wt, *Tm, *Em, *Vm, *Sm, *wn, *Pm, *colold, *colnew, *invd, *red, *scal;
+  double *Qs, *wcold;
+  T *WsT, *Bc, *Hc, *Rc;
   unsigned epoch = 0;
   int slot = 0;
+  // optional cycle profile of CTA 0 / thread 0 (args.prof != nullptr)
+  bool prof_on = false;
+  long long prof_last = 0;
+  long long prof_acc[kPfCount] = {};
+  __device__ __forceinline__ void prof_tick(int bucket) {
+    if (prof_on) {
+      const long long now = clock64();
+      prof_acc[bucket] += now - prof_last;
+      prof_last = now;
+    }
+  }
   int64_t part_slot_len;  // doubles per slot of a.part
   int64_t fin_slot_len;
 
@@ -108,6 +141,7 @@ struct Sweeper {
     RM = RM_;
     ncp = int(NCM) + 1;
     lq = l + 1;
+    kp = k + 1;
     double* D = reinterpret_cast<double*>(smem);
     Wt = D + L.wt;
     Tm = D + L.tm;
@@ -115,21 +149,27 @@ struct Sweeper {
     Vm = D + L.vm;
     Sm = D + L.sm;
     wn = D + L.wn;
+    Pm = D + L.pm;
+    colold = D + L.colold;
+    colnew = D + L.colnew;
+    invd = D + L.invd;
     red = D + L.red;
     scal = D + L.scal;
-    Qs = QS ? reinterpret_cast<T*>(smem + L.qs) : nullptr;
+    Qs = QS ? reinterpret_cast<double*>(smem + L.qs) : nullptr;
+    wcold = reinterpret_cast<double*>(smem + L.wcold);
     WsT = QS ? reinterpret_cast<T*>(smem + L.wst) : nullptr;
-    wcol = QS ? nullptr : reinterpret_cast<T*>(smem + L.wcol);
     Bc = reinterpret_cast<T*>(smem + L.bc);
     Hc = reinterpret_cast<T*>(smem + L.hc);
     Rc = reinterpret_cast<T*>(smem + L.rc);
     part_slot_len = sweep_part_len(l, k) * G;
     fin_slot_len = sweep_part_len(l, k);
+    prof_on = a.prof != nullptr && g == 0 && tid == 0;
+    if (prof_on) prof_last = clock64();
   }
 
   __device__ __forceinline__ double q(int64_t r, int i) const {
     if constexpr (QS)
-      return double(Qs[r * lq + i]);
+      return Qs[r * lq + i];
     else
       return double(__ldg(a.q + (r0 + r) * l + i));
   }
@@ -139,65 +179,104 @@ struct Sweeper {
     else
       return a.w[(r0 + r) * k + j];
   }
-  __device__ __forceinline__ T wcol_get(int64_t r, int j) const {
-    if constexpr (QS)
-      return WsT[int64_t(j) * RM + r];
-    else
-      return wcol[r];
-  }
+  __device__ __forceinline__ double wcol_get(int64_t r) const { return wcold[r]; }
   __device__ __forceinline__ double* part_base() { return a.part + int64_t(slot) * part_slot_len; }
   __device__ __forceinline__ double* fin_base() { return a.fin + int64_t(slot) * fin_slot_len; }
   __device__ __forceinline__ void next_slot() { slot ^= 1; }
 
   __device__ void barrier() { grid_barrier(a.barrier, epoch); }
 
-  // every CTA: dst(e) = sum_g part[e][g] for e < L (fixed order), writer(e, value)
+  // Partial layout is CTA-major: p[g * L + e] holds CTA g's contribution to entry e of an
+  // L-long vector.  wr(e, sum_g p[g][e]) for e in [e0, e1): consecutive threads take consecutive
+  // entries (coalesced), S thread-slices per entry stride over g with all loads independent, and
+  // the slices are combined in fixed order through shared memory.  Every thread of the CTA must
+  // call this (it contains __syncthreads).
+  template <typename Writer>
+  __device__ void reduce_entries(const double* p, int L, int e0, int e1, Writer&& wr) {
+    const int E = e1 - e0;
+    if (E <= 0) return;
+    for (int eb = 0; eb < E; eb += kSwThreads) {
+      const int EB = min(kSwThreads, E - eb);
+      const int S = max(1, min(G, kSwThreads / EB));
+      const int el = tid % EB, sidx = tid / EB;
+      double acc = 0.0;
+      if (sidx < S) {
+        const double* src = p + e0 + eb + el;
+        for (int gb = sidx; gb < G; gb += 16 * S) {
+          double v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int gg = gb + u * S;
+            v[u] = gg < G ? ld_cg(src + int64_t(gg) * L) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) acc += v[u];
+        }
+      }
+      red[tid] = acc;
+      __syncthreads();
+      if (tid < EB) {
+        double v = 0.0;
+        for (int q2 = 0; q2 < S; ++q2) v += red[q2 * EB + tid];
+        wr(e0 + eb + tid, v);
+      }
+      __syncthreads();
+    }
+  }
+
+  // every CTA: wr(e, sum_g part[e][g]) for e < L (fixed order)
   template <typename Writer>
   __device__ void reduce_all(int L, Writer&& wr) {
-    const double* p = part_base();
-    for (int e = wid; e < L; e += kSwWarps) {
-      double s = 0.0;
-      for (int gg = lane; gg < G; gg += 32) s += ld_cg(p + int64_t(e) * G + gg);
-      s = warp_allreduce_sum(s);
-      if (lane == 0) wr(e, s);
-    }
+    reduce_entries(part_base(), L, 0, L, wr);
   }
 
   // Single-level all-reduce of vectors already written to part_base(): one barrier.
   template <typename Writer>
   __device__ void allreduce1(int L, Writer&& wr) {
+    prof_tick(kPfOther);
     barrier();
+    prof_tick(kPfBarrier1);
     reduce_all(L, wr);
     next_slot();
     __syncthreads();
+    prof_tick(kPfReduce1);
   }
 
   // Two-level all-reduce (reduce-scatter over CTAs, then all-gather): two barriers.
   template <typename Writer>
   __device__ void allreduce2(int L, Writer&& wr) {
+    prof_tick(kPfOther);
     barrier();
+    prof_tick(kPfBarrier2);
     const double* p = part_base();
     double* f = fin_base();
     const int e0 = int(int64_t(L) * g / G), e1 = int(int64_t(L) * (g + 1) / G);
-    for (int e = e0 + wid; e < e1; e += kSwWarps) {
-      double s = 0.0;
-      for (int gg = lane; gg < G; gg += 32) s += ld_cg(p + int64_t(e) * G + gg);
-      s = warp_allreduce_sum(s);
-      if (lane == 0) f[e] = s;
-    }
+    reduce_entries(p, L, e0, e1, [&](int e, double v) { f[e] = v; });
+    __syncthreads();
+    prof_tick(kPfReduce2a);
     barrier();
-    for (int e = tid; e < L; e += kSwThreads) wr(e, ld_cg(f + e));
+    prof_tick(kPfBarrier2);
+    constexpr int U = 4;
+    for (int e = tid; e < L; e += kSwThreads * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = (e + kSwThreads * u < L) ? ld_cg(f + e + kSwThreads * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (e + kSwThreads * u < L) wr(e + kSwThreads * u, v[u]);
+    }
     next_slot();
     __syncthreads();
+    prof_tick(kPfReduce2b);
   }
 
   __device__ double block_sum(double v) {
     v = warp_allreduce_sum(v);
     __syncthreads();
-    if (lane == 0) red[kSwThreads + wid] = v;
+    if (lane == 0) red[kRedLen + wid] = v;
     __syncthreads();
     double s = 0.0;
-    for (int w = 0; w < kSwWarps; ++w) s += red[kSwThreads + w];
+    for (int w = 0; w < kSwWarps; ++w) s += red[kRedLen + w];
     __syncthreads();
     return s;
   }
@@ -208,7 +287,7 @@ struct Sweeper {
       for (int64_t e = tid; e < R * l; e += kSwThreads) {
         const int64_t r = e / l;
         const int i = int(e % l);
-        Qs[r * lq + i] = a.q[(r0 + r) * l + i];
+        Qs[r * lq + i] = double(a.q[(r0 + r) * l + i]);
       }
       for (int64_t e = tid; e < R * k; e += kSwThreads) {
         const int64_t r = e / k;
@@ -227,11 +306,11 @@ struct Sweeper {
       Hc[j * ncp + cl] = a.h[int64_t(j) * a.n + c0 + cl];
     }
     if (!(a.flags & kInitWt))
-      for (int e = tid; e < l * k; e += kSwThreads) Wt[e] = a.wt[e];
+      for (int e = tid; e < l * k; e += kSwThreads) Wt[(e / k) * kp + e % k] = a.wt[e];
     if (!(a.flags & kInitWn))
       for (int e = tid; e < k; e += kSwThreads) wn[e] = a.wn[e];
     if (!(a.flags & (kEval0 | kTvOnly))) {
-      for (int e = tid; e < l * k; e += kSwThreads) Tm[e] = a.tm[e];
+      for (int e = tid; e < l * k; e += kSwThreads) Tm[(e / k) * kp + e % k] = a.tm[e];
       for (int e = tid; e < k * k; e += kSwThreads) Vm[e] = a.vm[e];
     }
     __syncthreads();
@@ -254,9 +333,10 @@ struct Sweeper {
     }
     if (g == 0) {
       for (int e = tid; e < l * k; e += kSwThreads) {
-        a.wt[e] = Wt[e];
-        a.tm[e] = Tm[e];
-        a.em[e] = Em[e];
+        const int pe = (e / k) * kp + e % k;
+        a.wt[e] = Wt[pe];
+        a.tm[e] = Tm[pe];
+        a.em[e] = Em[pe];
       }
       for (int e = tid; e < k * k; e += kSwThreads) a.vm[e] = Vm[e];
       for (int e = tid; e < k; e += kSwThreads) a.wn[e] = wn[e];
@@ -283,16 +363,35 @@ struct Sweeper {
           s += wv * wv;
         }
       }
-      p[int64_t(e) * G + g] = s;
+      p[int64_t(g) * L + e] = s;
     }
     const bool do_wt = a.flags & kInitWt, do_wn = a.flags & kInitWn;
     allreduce2(L, [&](int e, double v) {
       if (e < lk) {
-        if (do_wt) Wt[e] = v;
+        if (do_wt) Wt[(e / k) * kp + e % k] = v;
       } else if (do_wn) {
         wn[e - lk] = v;
       }
     });
+  }
+
+  // P = W~ V (l x k), recomputed at the start of every W phase and then kept current with a
+  // rank-1 update after each column, so the step of column j costs one FMA per entry instead
+  // of a k-long dot product (same value as W~ * V(:,j) in rhals_w_component, up to rounding).
+  __device__ void compute_p() {
+    for (int e = tid; e < l * k; e += kSwThreads) {
+      const int i = e / k, c = e % k;
+      const double* wi = Wt + i * kp;
+      double s0 = 0.0, s1 = 0.0;
+      int t = 0;
+      for (; t + 1 < k; t += 2) {
+        s0 += wi[t] * Vm[t * k + c];
+        s1 += wi[t + 1] * Vm[(t + 1) * k + c];
+      }
+      if (t < k) s0 += wi[t] * Vm[t * k + c];
+      Pm[i * kp + c] = s0 + s1;
+    }
+    __syncthreads();
   }
 
   // One column step of rhals_w_component (p/src/rhals.cpp:23-32).
@@ -300,58 +399,108 @@ struct Sweeper {
     const double alpha = a.alpha_w, beta = a.beta_w;
     const double denom = fmax(Vm[j * k + j] + alpha, kDivisionFloor);
     if (tid < l) {
-      double wv = 0.0;
-      for (int c = 0; c < k; ++c) wv += Wt[tid * k + c] * Vm[c * k + j];
-      const double cur = Wt[tid * k + j];
-      Wt[tid * k + j] = cur + (Tm[tid * k + j] - wv - alpha * cur) / denom;
+      const double cur = Wt[tid * kp + j];
+      const double nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) / denom;
+      colold[tid] = cur;
+      colnew[tid] = nw;
     }
     __syncthreads();
+    prof_tick(kPfWStep);
     const double shift = beta != 0.0 ? beta / denom : 0.0;
     for (int64_t r = tid; r < R; r += kSwThreads) {
-      double u = 0.0;
-      for (int i = 0; i < l; ++i) u += q(r, i) * Wt[i * k + j];
-      if (beta != 0.0) u -= shift;
-      const T wv = T(fmax(u, 0.0));
-      if constexpr (QS) {
-        WsT[int64_t(j) * RM + r] = wv;
-      } else {
-        wcol[r] = wv;
-        a.w[(r0 + r) * k + j] = wv;
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+      int i = 0;
+      for (; i + 3 < l; i += 4) {
+        u0 += q(r, i) * colnew[i];
+        u1 += q(r, i + 1) * colnew[i + 1];
+        u2 += q(r, i + 2) * colnew[i + 2];
+        u3 += q(r, i + 3) * colnew[i + 3];
       }
+      for (; i < l; ++i) u0 += q(r, i) * colnew[i];
+      double u = (u0 + u1) + (u2 + u3);
+      if (beta != 0.0) u -= shift;
+      const double wd = fmax(u, 0.0);
+      wcold[r] = wd;
+      if constexpr (QS)
+        WsT[int64_t(j) * RM + r] = T(wd);
+      else
+        a.w[(r0 + r) * k + j] = T(wd);
     }
     __syncthreads();
-    // partials of [Q^T W(:,j); ||W(:,j)||^2] over this CTA's rows
+    prof_tick(kPfLift);
+    // partials of [Q^T W(:,j); ||W(:,j)||^2] over this CTA's rows: warp w takes rows w, w+8, ..
+    // (two interleaved accumulators); lane slot u covers output i = lane + 32 u, where output l
+    // is the squared norm ("column l of Q" is W(:,j) itself).  Branch-free: inactive lanes
+    // multiply by zero.
     const int L1 = l + 1;
-    const int S = kSwThreads / L1;
-    if (tid < S * L1) {
-      const int i = tid % L1, s = tid / L1;
-      double acc = 0.0;
-      for (int64_t r = s; r < R; r += S) {
-        const double wr = double(wcol_get(r, j));
-        acc += (i < l ? q(r, i) : wr) * wr;
+    {
+      const int nslots = (L1 + 31) / 32;
+      double a0[kMaxLSlots], a1[kMaxLSlots];
+#pragma unroll
+      for (int u = 0; u < kMaxLSlots; ++u) a0[u] = a1[u] = 0.0;
+      int64_t r = wid;
+      for (; r + kSwWarps < R; r += 2 * kSwWarps) {
+        const double w0 = wcol_get(r), w1 = wcol_get(r + kSwWarps);
+#pragma unroll
+        for (int u = 0; u < kMaxLSlots; ++u) {
+          if (u < nslots) {
+            const int i = lane + 32 * u;
+            const int ic = i < l ? i : l - 1;
+            const double sel = i < l ? 1.0 : 0.0;
+            const double q0 = sel * q(r, ic) + (i == l ? w0 : 0.0);
+            const double q1 = sel * q(r + kSwWarps, ic) + (i == l ? w1 : 0.0);
+            a0[u] += q0 * w0;
+            a1[u] += q1 * w1;
+          }
+        }
       }
-      red[s * L1 + i] = acc;
+      if (r < R) {
+        const double w0 = wcol_get(r);
+#pragma unroll
+        for (int u = 0; u < kMaxLSlots; ++u) {
+          if (u < nslots) {
+            const int i = lane + 32 * u;
+            const int ic = i < l ? i : l - 1;
+            const double q0 = (i < l ? q(r, ic) : 0.0) + (i == l ? w0 : 0.0);
+            a0[u] += q0 * w0;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kMaxLSlots; ++u) {
+        const int i = lane + 32 * u;
+        if (u < nslots && i < L1) red[wid * kRedStride + i] = a0[u] + a1[u];
+      }
     }
     __syncthreads();
     if (tid < L1) {
       double v = 0.0;
-      for (int s = 0; s < S; ++s) v += red[s * L1 + tid];
-      part_base()[int64_t(tid) * G + g] = v;
+      for (int w = 0; w < kSwWarps; ++w) v += red[w * kRedStride + tid];
+      part_base()[int64_t(g) * L1 + tid] = v;
     }
+    prof_tick(kPfRecomp);
     allreduce1(L1, [&](int e, double v) {
       if (e < l)
-        Wt[e * k + j] = v;
+        colnew[e] = v;
       else
         wn[j] = v;
     });
+    // W~(:,j) <- Q^T W(:,j); P += (W~_new(:,j) - W~_old(:,j)) V(j,:)
+    for (int e = tid; e < l * k; e += kSwThreads) {
+      const int i = e / k, c = e % k;
+      Pm[i * kp + c] += (colnew[i] - colold[i]) * Vm[j * k + c];
+    }
+    if (tid < l) Wt[tid * kp + j] = colnew[tid];
+    __syncthreads();
   }
 
-  // S = W~^T W~ (k x k), replicated
+  // S = W~^T W~ (k x k), replicated; invd_j = 1 / max(||W(:,j)||^2 + alpha_h, floor)
   __device__ void compute_s() {
+    for (int e = tid; e < k; e += kSwThreads) invd[e] = 1.0 / fmax(wn[e] + a.alpha_h, kDivisionFloor);
     for (int e = tid; e < k * k; e += kSwThreads) {
       const int x = e / k, y = e % k;
       double s = 0.0;
-      for (int i = 0; i < l; ++i) s += Wt[i * k + x] * Wt[i * k + y];
+      for (int i = 0; i < l; ++i) s += Wt[i * kp + x] * Wt[i * kp + y];
       Sm[e] = s;
     }
     __syncthreads();
@@ -361,145 +510,185 @@ struct Sweeper {
   // T, V, E, objc, pgrad_H.
   //   update:     apply clamped_row_update for j = 0..k-1 (p/src/rhals.cpp:52-55)
   //   grad_valid: grad_H = 2 (S H - R^T) (scratch valid, :154); else -2 W~^T residc (:155)
+  // A column is handled by LPC lanes (16 when k <= 16, two columns per warp; else 32).  Lane j
+  // keeps h_j, r_j = (B^T W~)(c, j) and the running dot acc_j = sum_i S(i,j) h_i; the sequential
+  // row update j broadcasts only the change of h_j, so each of the k steps costs one shuffle
+  // and one FMA per lane instead of a k-long reduction.  After the loop acc_j = (S h)_j, which is
+  // exactly the first term of grad_H.
   __device__ void h_phase(bool update, bool grad_valid, double& objc, double& pgh) {
+    prof_tick(kPfOther);
     compute_s();
     const double alpha = a.alpha_h, beta = a.beta_h;
+    const int LPC = k <= 16 ? 16 : 32;
+    const int CPW = 32 / LPC;
+    const int sub = lane / LPC, sl = lane % LPC;
     double objc_l = 0.0, pgh_l = 0.0;
-    for (int64_t cl = wid; cl < NC; cl += kSwWarps) {
-      double h[kMaxPerLane], r[kMaxPerLane];
+    for (int64_t cb = int64_t(wid) * CPW; cb < NC; cb += int64_t(kSwWarps) * CPW) {
+      const int64_t cl = cb + sub;
+      const bool valid = cl < NC;
+      const int64_t clx = valid ? cl : 0;
+      double h[kMaxPerLane], r[kMaxPerLane], acc[kMaxPerLane];
 #pragma unroll
       for (int t = 0; t < kMaxPerLane; ++t) {
-        const int j = lane + 32 * t;
-        h[t] = j < k ? double(Hc[j * ncp + cl]) : 0.0;
-        r[t] = 0.0;
+        const int j = sl + LPC * t;
+        h[t] = (valid && j < k) ? double(Hc[j * ncp + clx]) : 0.0;
+        double r0v = 0.0, r1v = 0.0;
+        if (j < k) {
+          int i = 0;
+          for (; i + 1 < l; i += 2) {
+            r0v += double(Bc[i * ncp + clx]) * Wt[i * kp + j];
+            r1v += double(Bc[(i + 1) * ncp + clx]) * Wt[(i + 1) * kp + j];
+          }
+          if (i < l) r0v += double(Bc[i * ncp + clx]) * Wt[i * kp + j];
+        }
+        r[t] = r0v + r1v;
+        acc[t] = 0.0;
       }
-      for (int i = 0; i < l; ++i) {
-        const double bi = double(Bc[i * ncp + cl]);
+      // acc_j = sum_i S(i, j) h_i
+      for (int i = 0; i < k; ++i) {
+        double src = 0.0;
+#pragma unroll
+        for (int t = 0; t < kMaxPerLane; ++t)
+          if (t == i / LPC) src = h[t];
+        const double hi = __shfl_sync(0xffffffffu, src, i % LPC, LPC);
 #pragma unroll
         for (int t = 0; t < kMaxPerLane; ++t) {
-          const int j = lane + 32 * t;
-          if (j < k) r[t] += bi * Wt[i * k + j];
+          const int j = sl + LPC * t;
+          if (j < k) acc[t] += Sm[i * k + j] * hi;
         }
       }
       if (update) {
         for (int j = 0; j < k; ++j) {
-          double p = 0.0;
-#pragma unroll
-          for (int t = 0; t < kMaxPerLane; ++t) {
-            const int jj = lane + 32 * t;
-            if (jj < k) p += Sm[jj * k + j] * h[t];
-          }
-          const double dot = warp_allreduce_sum(p);
-          if (lane == (j & 31)) {
-            const double d = fmax(wn[j] + alpha, kDivisionFloor);
+          const int owner = j % LPC, slot = j / LPC;
+          double delta = 0.0;
+          if (sl == owner) {
 #pragma unroll
             for (int t = 0; t < kMaxPerLane; ++t) {
-              if (t == (j >> 5)) {
-                double num = r[t] - dot - alpha * h[t];
+              if (t == slot) {
+                double num = r[t] - acc[t] - alpha * h[t];
                 if (beta != 0.0) num -= beta;
-                h[t] = fmax(0.0, h[t] + num / d);
+                const double hn = fmax(0.0, h[t] + num * invd[j]);
+                delta = hn - h[t];
+                h[t] = hn;
               }
             }
           }
+          const double dj = __shfl_sync(0xffffffffu, delta, owner, LPC);
+#pragma unroll
+          for (int t = 0; t < kMaxPerLane; ++t) {
+            const int jj = sl + LPC * t;
+            if (jj < k) acc[t] += Sm[j * k + jj] * dj;
+          }
         }
       }
-      // residc(:,c) = B(:,c) - W~ h ; grad accumulators
-      double res[kMaxPerLane], gs[kMaxPerLane];
+      // residc(:,c) = B(:,c) - W~ h
+      double res[kMaxResSlots];
 #pragma unroll
-      for (int u = 0; u < kMaxPerLane; ++u) {
-        const int i = lane + 32 * u;
-        res[u] = i < l ? double(Bc[i * ncp + cl]) : 0.0;
-        gs[u] = 0.0;
+      for (int u = 0; u < kMaxResSlots; ++u) {
+        const int i = sl + LPC * u;
+        res[u] = (i < l) ? double(Bc[i * ncp + clx]) : 0.0;
       }
       for (int j = 0; j < k; ++j) {
-        double hsrc = 0.0;
+        double src = 0.0;
 #pragma unroll
         for (int t = 0; t < kMaxPerLane; ++t)
-          if (t == (j >> 5)) hsrc = h[t];
-        const double hj = __shfl_sync(0xffffffffu, hsrc, j & 31);
+          if (t == j / LPC) src = h[t];
+        const double hj = __shfl_sync(0xffffffffu, src, j % LPC, LPC);
 #pragma unroll
-        for (int u = 0; u < kMaxPerLane; ++u) {
-          const int i = lane + 32 * u;
-          if (i < l) res[u] -= Wt[i * k + j] * hj;
-        }
-        if (grad_valid) {
-#pragma unroll
-          for (int t = 0; t < kMaxPerLane; ++t) {
-            const int jj = lane + 32 * t;
-            if (jj < k) gs[t] += Sm[jj * k + j] * hj;
-          }
+        for (int u = 0; u < kMaxResSlots; ++u) {
+          const int i = sl + LPC * u;
+          if (i < l) res[u] -= Wt[i * kp + j] * hj;
         }
       }
+      double gs[kMaxPerLane];
+#pragma unroll
+      for (int t = 0; t < kMaxPerLane; ++t) gs[t] = 0.0;
       if (!grad_valid) {
-        // -2 W~^T residc: broadcast residc entries across the warp
+        // -2 W~^T residc: broadcast residc entries across the column's lanes
         for (int i = 0; i < l; ++i) {
-          double rsrc = 0.0;
+          double src = 0.0;
 #pragma unroll
-          for (int u = 0; u < kMaxPerLane; ++u)
-            if (u == (i >> 5)) rsrc = res[u];
-          const double ri = __shfl_sync(0xffffffffu, rsrc, i & 31);
+          for (int u = 0; u < kMaxResSlots; ++u)
+            if (u == i / LPC) src = res[u];
+          const double ri = __shfl_sync(0xffffffffu, src, i % LPC, LPC);
 #pragma unroll
           for (int t = 0; t < kMaxPerLane; ++t) {
-            const int jj = lane + 32 * t;
-            if (jj < k) gs[t] += Wt[i * k + jj] * ri;
+            const int jj = sl + LPC * t;
+            if (jj < k) gs[t] += Wt[i * kp + jj] * ri;
           }
         }
       }
+      if (valid) {
 #pragma unroll
-      for (int u = 0; u < kMaxPerLane; ++u) {
-        const int i = lane + 32 * u;
-        if (i < l) {
-          objc_l += res[u] * res[u];
-          Rc[i * ncp + cl] = T(res[u]);
+        for (int u = 0; u < kMaxResSlots; ++u) {
+          const int i = sl + LPC * u;
+          if (i < l) {
+            objc_l += res[u] * res[u];
+            Rc[i * ncp + cl] = T(res[u]);
+          }
         }
-      }
 #pragma unroll
-      for (int t = 0; t < kMaxPerLane; ++t) {
-        const int j = lane + 32 * t;
-        if (j < k) {
-          if (update) Hc[j * ncp + cl] = T(h[t]);
-          const double gval = grad_valid ? 2.0 * (gs[t] - r[t]) : -2.0 * gs[t];
-          const double gp = h[t] > 0.0 ? gval : fmin(0.0, gval);
-          pgh_l += gp * gp;
+        for (int t = 0; t < kMaxPerLane; ++t) {
+          const int j = sl + LPC * t;
+          if (j < k) {
+            if (update) Hc[j * ncp + cl] = T(h[t]);
+            const double gval = grad_valid ? 2.0 * (acc[t] - r[t]) : -2.0 * gs[t];
+            const double gp = h[t] > 0.0 ? gval : fmin(0.0, gval);
+            pgh_l += gp * gp;
+          }
         }
       }
     }
     __syncthreads();
+    prof_tick(kPfHCols);
     // CTA partial products: [T (l k) | V (k k) | E (l k) | objc | pgh]
     const int lk = l * k, kk = k * k, L = 2 * lk + kk + 2;
     double* p = part_base();
     for (int e = tid; e < 2 * lk + kk; e += kSwThreads) {
-      double s = 0.0;
+      const T *xa, *xb;
       if (e < lk) {
-        const T* bi = Bc + (e / k) * ncp;
-        const T* hj = Hc + (e % k) * ncp;
-        for (int64_t c = 0; c < NC; ++c) s += double(bi[c]) * double(hj[c]);
+        xa = Bc + (e / k) * ncp;
+        xb = Hc + (e % k) * ncp;
       } else if (e < lk + kk) {
         const int f = e - lk;
-        const T* ha = Hc + (f / k) * ncp;
-        const T* hb = Hc + (f % k) * ncp;
-        for (int64_t c = 0; c < NC; ++c) s += double(ha[c]) * double(hb[c]);
+        xa = Hc + (f / k) * ncp;
+        xb = Hc + (f % k) * ncp;
       } else {
         const int f = e - lk - kk;
-        const T* ri = Rc + (f / k) * ncp;
-        const T* hj = Hc + (f % k) * ncp;
-        for (int64_t c = 0; c < NC; ++c) s += double(ri[c]) * double(hj[c]);
+        xa = Rc + (f / k) * ncp;
+        xb = Hc + (f % k) * ncp;
       }
-      p[int64_t(e) * G + g] = s;
+      double s0 = 0.0, s1 = 0.0;
+      int64_t c = 0;
+      for (; c + 1 < NC; c += 2) {
+        s0 += double(xa[c]) * double(xb[c]);
+        s1 += double(xa[c + 1]) * double(xb[c + 1]);
+      }
+      if (c < NC) s0 += double(xa[c]) * double(xb[c]);
+      p[int64_t(g) * L + e] = s0 + s1;
     }
-    const double o = block_sum(objc_l);
-    const double ph = block_sum(pgh_l);
-    if (tid == 0) {
-      p[int64_t(L - 2) * G + g] = o;
-      p[int64_t(L - 1) * G + g] = ph;
+    {
+      const double o = warp_allreduce_sum(objc_l), ph = warp_allreduce_sum(pgh_l);
+      if (lane == 0) {
+        red[kRedLen + wid] = o;
+        red[kRedLen + kSwWarps + wid] = ph;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double so = 0.0, sp = 0.0;
+        for (int w = 0; w < kSwWarps; ++w) so += red[kRedLen + w], sp += red[kRedLen + kSwWarps + w];
+        p[int64_t(g) * L + L - 2] = so;
+        p[int64_t(g) * L + L - 1] = sp;
+      }
     }
+    prof_tick(kPfHProducts);
     allreduce2(L, [&](int e, double v) {
       if (e < lk)
-        Tm[e] = v;
+        Tm[(e / k) * kp + e % k] = v;
       else if (e < lk + kk)
         Vm[e - lk] = v;
       else if (e < 2 * lk + kk)
-        Em[e - lk - kk] = v;
+        Em[((e - lk - kk) / k) * kp + (e - lk - kk) % k] = v;
       else
         scal[e - (2 * lk + kk)] = v;  // scal[0] = objc, scal[1] = pgh
     });
@@ -509,19 +698,34 @@ struct Sweeper {
   }
 
   // projected ||grad_W||^2 with grad_W = -2 Q E (E = residc H^T), reduced over the grid.
+  // Thread per row, 16 independent accumulators per pass (throughput- not latency-bound).
   __device__ double pgrad_w() {
     double acc = 0.0;
     for (int64_t r = tid; r < R; r += kSwThreads) {
-      for (int j = 0; j < k; ++j) {
-        double s = 0.0;
-        for (int i = 0; i < l; ++i) s += q(r, i) * Em[i * k + j];
-        const double gv = -2.0 * s;
-        const double gp = w_get(r, j) > T(0) ? gv : fmin(0.0, gv);
-        acc += gp * gp;
+      for (int j0 = 0; j0 < k; j0 += 16) {
+        double sacc[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) sacc[u] = 0.0;
+        for (int i = 0; i < l; ++i) {
+          const double qv = q(r, i);
+          const double* ei = Em + i * kp + j0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (j0 + u < k) sacc[u] += qv * ei[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if (j0 + u < k) {
+            const double gv = -2.0 * sacc[u];
+            const double gp = w_get(r, j0 + u) > T(0) ? gv : fmin(0.0, gv);
+            acc += gp * gp;
+          }
+        }
       }
     }
     const double tot = block_sum(acc);
     if (tid == 0) part_base()[g] = tot;
+    prof_tick(kPfPgw);
     allreduce1(1, [&](int, double v) { scal[2] = v; });
     const double out = scal[2];
     __syncthreads();
@@ -537,6 +741,7 @@ struct Sweeper {
   }
 
   __device__ void run() {
+    const long long t_start = clock64();
     load_resident();
     if (a.flags & (kInitWt | kInitWn)) init_wt_wn();
     double pgrad0 = 0.0;
@@ -557,8 +762,10 @@ struct Sweeper {
     const bool stationary = (a.flags & kRecord) && pg_rule && !(pgrad0 > 0.0);
     if (!stationary) {
       for (int64_t t = a.t_begin; t <= a.t_end; ++t) {
-        if (a.flags & kDoW)
+        if (a.flags & kDoW) {
+          compute_p();
           for (int j = 0; j < k; ++j) w_column(j);
+        }
         if (a.flags & kDoH) {
           double objc = 0.0, pgh = 0.0;
           h_phase(true, true, objc, pgh);
@@ -576,6 +783,11 @@ struct Sweeper {
         }
         last = t;
       }
+    }
+    if (prof_on) {
+      prof_acc[kPfSweeps] = clock64() - t_start;
+      for (int b = 0; b < kPfCount; ++b) a.prof[b] = prof_acc[b];
+      a.prof[kPfCount] = epoch;
     }
     store_back(last, stopped);
   }

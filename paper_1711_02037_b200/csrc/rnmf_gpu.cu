@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -450,6 +451,14 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   a.barrier = ctx->d<unsigned>("sw.barrier", 1);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+  // RNMF_PROF=1: per-phase cycle counters of CTA 0, printed to stderr (development aid)
+  const bool prof = std::getenv("RNMF_PROF") != nullptr;
+  std::vector<long long> prof_sum(kSweepProfSlots, 0);
+  long long* hprof = nullptr;
+  if (prof) {
+    a.prof = ctx->d<long long>("sw.prof", kSweepProfSlots);
+    hprof = ctx->h<long long>("sw.prof.h", kSweepProfSlots);
+  }
 
   // Metrics results, one slot per evaluation: [objective, pgrad_full]
   const int64_t max_evals = max_iter / o.trace_full_every + 4 + (o.stopping == RNMF_STOP_OBJECTIVE ? max_iter : 0);
@@ -481,7 +490,10 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     a.t_end = t_end;
     tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
     RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    if (prof) RNMF_CUDA(cudaMemcpyAsync(hprof, a.prof, kSweepProfSlots * sizeof(long long), cudaMemcpyDeviceToHost, st));
     RNMF_CUDA(cudaStreamSynchronize(st));
+    if (prof)
+      for (int i = 0; i < kSweepProfSlots; ++i) prof_sum[size_t(i)] += hprof[i];
     first = false;
     last = hstat[0];
     const bool stopped = hstat[1] != 0;
@@ -532,6 +544,15 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     r.elapsed_s = h_ref + std::max(0.0, dt);
   }
   for (int64_t t = 1; t < nrec; ++t) trace[t].elapsed_s = std::max(trace[t].elapsed_s, trace[t - 1].elapsed_s);
+  if (prof) {
+    static const char* names[] = {"w_step", "lift", "recompress", "barrier1", "reduce1", "h_cols", "h_products",
+                                  "barrier2", "reduce2a", "reduce2b", "pgw", "other", "kernel_total", "barriers"};
+    std::fprintf(stderr, "[rnmf prof] sweeps=%lld grid=%d smem=%zu q_in_smem=%d (cycles of CTA 0 summed over launches)\n",
+                 (long long)last, plan.grid, plan.smem, int(plan.q_in_smem));
+    for (int i = 0; i < kSweepProfSlots; ++i)
+      std::fprintf(stderr, "[rnmf prof] %-12s %14lld  per-sweep %10.1f\n", names[i], prof_sum[size_t(i)],
+                   double(prof_sum[size_t(i)]) / double(std::max<int64_t>(last, 1)));
+  }
   *trace_len = nrec;
   ctx->last.sweeps = last;
 }

@@ -32,14 +32,17 @@ def _rel(a, b, floor=1e-300):
     return abs(a - b) / max(abs(b), floor)
 
 
-def assert_trace_close(gpu_trace, ora_trace, rtol, final_atol=None, fields=("rel_err", "objective_compressed", "objective")):
+def assert_trace_close(gpu_trace, ora_trace, rtol, final_atol=None, fields=("rel_err", "objective_compressed", "objective"),
+                       floor=1e-10):
+    """Per-record relative check; `floor` (relative to the field's largest value over the trace)
+    absorbs fields that converge to rounding level (e.g. an exactly fitted compressed residual)."""
     assert len(gpu_trace) == len(ora_trace), (len(gpu_trace), len(ora_trace))
-    for g, o in zip(gpu_trace, ora_trace):
-        assert g.iter == o["iter"]
-        for f in fields:
+    for f in fields:
+        atol = floor * max(abs(o[f]) for o in ora_trace)
+        for g, o in zip(gpu_trace, ora_trace):
+            assert g.iter == o["iter"]
             gv, ov = getattr(g, f), o[f]
-            scale = max(abs(ov), 1e-300)
-            assert abs(gv - ov) <= rtol * scale, f"iter {o['iter']} {f}: gpu {gv!r} oracle {ov!r}"
+            assert abs(gv - ov) <= rtol * abs(ov) + atol, f"iter {o['iter']} {f}: gpu {gv!r} oracle {ov!r}"
     if final_atol is not None:
         assert abs(gpu_trace[-1].rel_err - ora_trace[-1]["rel_err"]) <= final_atol
 
@@ -139,3 +142,92 @@ def test_max_iter_zero_returns_init(gpu, oracle):
     w, h = oracle.init_factors(x, 2, 0, 55)
     np.testing.assert_allclose(res.factors.w, w, rtol=1e-15)
     np.testing.assert_allclose(res.factors.h, h, rtol=1e-15)
+
+
+@pytest.mark.parametrize("shape", [(400, 200, 6, 6), (2000, 1000, 20, 10)])
+def test_rank_deficient_two_stage(gpu, oracle, shape):
+    """Config-1 style exact low rank r < l: the trailing l - r columns of Q are rounding noise, so
+    parity is checked in two stages: (a) the sketch captures range(X) exactly,
+    (b) the GPU sweep loop started from the oracle's compressed problem matches the oracle's loop;
+    (c) the end-to-end final rel_err agrees to the BASELINE 1e-4 absolute bar."""
+    m, n, r, p = shape
+    x = workloads.c1_matrix(1, m, n, r)
+    l = r + p
+    om, w0, h0 = workloads.injected_inputs(5, m, n, r, l)
+    # (a)
+    sk = gpu.rqb(x, gpu.SketchOptions(target_rank=r, oversampling=p, power_iterations=2), omega=om)
+    assert np.linalg.norm(x - sk.q @ sk.b) <= 1e-10 * np.linalg.norm(x)
+    assert np.abs(sk.q.T @ sk.q - np.eye(l)).max() <= 1e-12
+    # (b)
+    o = _opts(gpu, rank=r, max_iter=100, tol=1e-300, oversampling=p, power_iterations=2, seed=0)
+    cp = oracle.compress(x, _odict(o), omega=om, w0=w0, h0=h0)
+    ref = oracle.rhals_fit_compressed(x, _odict(o), cp)
+    gcp = gpu.CompressedProblem(cp.q.copy(), cp.b.copy(), cp.wt.copy(), cp.w.copy(), cp.h.copy())
+    res = gpu.rhals_fit_compressed(x, o, gcp)
+    assert_trace_close(res.trace, ref.trace, 1e-7)
+    # (c) un-injected end to end: the gap is set by the rounding-noise completion of Q; the BASELINE
+    # bar is asserted on the real C1 shape and only reported on the small one.
+    e2e_ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    e2e = gpu.rhals_fit(x, o, omega=om, w0=w0, h0=h0)
+    gap = abs(e2e.trace[-1].rel_err - e2e_ref.trace[-1]["rel_err"])
+    print(f"rank-deficient {m}x{n} r={r} l={l}: end-to-end final rel_err gap {gap:.3e}")
+    if (m, n) == (2000, 1000):
+        assert gap <= 1e-4
+
+
+def test_torch_device_inputs(gpu, oracle):
+    """X as a CUDA tensor: device-resident input and outputs (RNMF_DEVICE location)."""
+    import torch
+
+    x = oracle.synth_lowrank(300, 140, 5, 0.1, 3)
+    o = _opts(gpu, rank=5, max_iter=15, tol=1e-300, oversampling=5, seed=1)
+    ref = gpu.rhals_fit(x.astype(np.float32), o)
+    xd = torch.from_numpy(x.astype(np.float32)).cuda()
+    res = gpu.rhals_fit(xd, o)
+    assert res.factors.w.is_cuda and res.factors.w.dtype == torch.float32
+    np.testing.assert_array_equal(res.factors.w.cpu().numpy(), ref.factors.w)
+    np.testing.assert_array_equal(res.factors.h.cpu().numpy(), ref.factors.h)
+    assert [t.objective_compressed for t in res.trace] == [t.objective_compressed for t in ref.trace]
+
+
+def test_deterministic(gpu, oracle):
+    x = oracle.synth_lowrank(500, 300, 6, 0.1, 8).astype(np.float32)
+    o = _opts(gpu, rank=6, max_iter=12, tol=1e-300, oversampling=6, seed=4)
+    a = gpu.rhals_fit(x, o)
+    b = gpu.rhals_fit(x, o)
+    np.testing.assert_array_equal(a.factors.w, b.factors.w)
+    np.testing.assert_array_equal(a.factors.h, b.factors.h)
+    assert [t.pgrad for t in a.trace] == [t.pgrad for t in b.trace]
+
+
+@pytest.mark.parametrize("m,n,k,p", [(37, 1000, 3, 2), (5000, 40, 7, 9), (151, 149, 1, 0), (300, 31, 30, 1), (1, 1, 1, 0)])
+def test_ragged_and_edge_shapes(gpu, oracle, m, n, k, p):
+    """Row/column counts below, around and not multiples of the grid (148) and tile sizes;
+    k = min(m, n) (clamped sketch), rank 1, a 1 x 1 problem."""
+    rng = np.random.default_rng(m * 7 + n)
+    x = np.abs(rng.standard_normal((m, n))) + 0.1
+    # a 1 x 1 problem is fitted exactly after one sweep; later pgrads are rounding noise
+    o = _opts(gpu, rank=k, max_iter=1 if m * n == 1 else 8, tol=1e-300, oversampling=p, seed=3)
+    l = min(k + p, m, n)
+    om, w0, h0 = workloads.injected_inputs(2, m, n, k, l)
+    ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    res = gpu.rhals_fit(x, o, omega=om, w0=w0, h0=h0)
+    assert_trace_close(res.trace, ref.trace, 1e-7)
+
+
+def test_objective_stopping_rule(gpu, oracle):
+    x = oracle.synth_lowrank(80, 60, 3, 0.01, 4)
+    o = _opts(gpu, rank=3, max_iter=300, tol=2.0, stopping=gpu.StoppingRule.Objective, oversampling=5, seed=6)
+    ref = oracle.rhals_fit(x, _odict(o))
+    res = gpu.rhals_fit(x, o)
+    assert len(res.trace) == len(ref.trace) < 301
+    assert_trace_close(res.trace, ref.trace, 1e-7)
+
+
+def test_stage_shape_errors(gpu):
+    q, b, wt, w, h = np.zeros((10, 4)), np.zeros((4, 8)), np.zeros((4, 2)), np.zeros((10, 2)), np.zeros((3, 8))
+    cp = gpu.CompressedProblem(q, b, wt, w, h)
+    with pytest.raises(gpu.ShapeError, match="inconsistent compressed problem"):
+        gpu.rhals_update_W(cp)
+    with pytest.raises(gpu.ShapeError):
+        gpu.rhals_update_H(cp)
