@@ -19,14 +19,14 @@ int launch_scan(const T* x, int64_t count, unsigned long long* bad, double* part
 // ---- X-streaming GEMMs (kernels_xgemm.cu) ----------------------------------------------------
 // Y (m x c) = X (m x n) * S (n x c).  All row-major, leading dims = column counts.
 template <typename T>
-int launch_xw(const T* x, int64_t m, int64_t n, const T* s, int c, T* y, cudaStream_t stream);
+int launch_xw(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* y, cudaStream_t stream);
 
 // Fused full-space metrics pass 1 over X: with S = H^T (n x k) and W (m x k):
 //   part_obj[b]  = partial sum of (X - W H)^2 over CTA b's rows
 //   part_pgw[b]  = partial sum of projected (grad_W)^2, grad_W = -2 (X H^T - W (H H^T))
 // hht: k x k fp64.  Returns launches; *nblocks receives the number of partials written.
 template <typename T>
-int launch_xw_metrics(const T* x, int64_t m, int64_t n, const T* ht, const T* w, int k,
+int launch_xw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* ht, const T* w, int k,
                       const double* hht, double* part_obj, double* part_pgw, int* nblocks,
                       cudaStream_t stream);
 int xw_metrics_blocks(int64_t m);
@@ -35,14 +35,17 @@ int xw_metrics_blocks(int64_t m);
 // splits * n * c values of T), then reduced in fixed order into `out` (n x c, or c x n when
 // transpose_out).  splits = 0 picks a default.
 template <typename T>
-int launch_xtw(const T* x, int64_t m, int64_t n, const T* s, int c, T* part, int splits, T* out,
+int launch_xtw(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* part, int splits, T* out,
                bool transpose_out, cudaStream_t stream);
+// fixed-order reduction of split partials part[s][n][c] -> out (n x c, or c x n)
+template <typename T>
+int launch_splitk_reduce(const T* part, int splits, int64_t n, int c, T* out, bool transpose_out, cudaStream_t stream);
 int xtw_default_splits(int64_t m, int64_t n);
 
 // Metrics pass 2: with S = W (m x k): part_pgh[b] = partial sums of projected (grad_H)^2,
 // grad_H = -2 (W^T X - (W^T W) H), wtw: k x k fp64.  part holds splits*n*k values of T.
 template <typename T>
-int launch_xtw_metrics(const T* x, int64_t m, int64_t n, const T* w, int k, const T* h,
+int launch_xtw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w, int k, const T* h,
                        const double* wtw, T* part, int splits, double* part_pgh, int* nblocks,
                        cudaStream_t stream);
 
@@ -68,6 +71,21 @@ int launch_sum_parts(const double* part, int count, double* out, cudaStream_t st
 // writes %globaltimer to *out
 int launch_timestamp(unsigned long long* out, cudaStream_t stream);
 
+// ---- tcgen05 tensor-core X-streaming GEMMs (kernels_tc.cu, fp32 X only) ------------------------
+int tc_npad(int c);               // UMMA N for c output columns (multiple of 16)
+int64_t tc_st_pitch(int64_t n);   // pitch of the S^T operand
+// S (n x c) -> S^T split into tf32 hi and fp32 lo parts (tc_npad(c) x tc_st_pitch(n) each)
+int launch_tc_prep_st(const float* s, int64_t n, int c, float* st_hi, float* st_lo, cudaStream_t stream);
+// Y (m x c) = X (m x n, pitch ldx) * S; x3 = 3xTF32 (fp32-accurate), else 1xTF32
+int launch_tc_xw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo, int c,
+                 float* y, bool x3, int sm_count, cudaStream_t stream);
+
+// part[split] (n x c) = X[rows of split]^T S[rows of split]; S^T given as st (tc_npad(c) x
+// tc_st_pitch(m), K-major).  The caller reduces the splits.
+int tc_xtw_splits(int64_t m, int64_t n, int sm_count);
+int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, int c, float* part, int splits,
+                  int sm_count, cudaStream_t stream);
+
 // ---- tall-skinny QR (kernels_tsqr.cu) ---------------------------------------------------------
 // Householder TSQR of A (rows x l, row-major) -> explicit thin Q (rows x l, written to q_out in
 // T).  Workspace sized by tsqr_workspace_doubles.  Requires rows >= l.
@@ -76,6 +94,13 @@ template <typename T>
 int launch_tsqr(const T* a, int64_t rows, int l, T* q_out, double* ws, int max_smem,
                 cudaStream_t stream);
 int tsqr_max_l(int max_smem);
+
+// ---- CholeskyQR2 fast path (kernels_cholqr.cu) -------------------------------------------------
+// Q (rows x l) of A via two fp64-Gram CholeskyQR passes; *flag (device) is set non-zero when A is
+// too ill-conditioned for CholeskyQR2 (the caller then runs TSQR).  l <= 128.
+int64_t cholqr_workspace_doubles(int64_t rows, int l);
+template <typename T>
+int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream);
 
 // ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cu) -----------------------------
 enum SweepFlags : int {

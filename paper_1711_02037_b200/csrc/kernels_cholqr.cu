@@ -1,0 +1,223 @@
+// kernels_cholqr.cu — CholeskyQR2 fast path for the sketch's thin QRs (economic_qr,
+// p/src/core.cpp:7-16, called at p/src/sketch.cpp:62,63,68), with Householder TSQR as the fallback.
+//
+// Any orthonormal basis of range(A) is a valid replacement for Eigen's Householder Q (rHALS depends
+// only on range(Q), SURVEY §0 finding 4).  CholeskyQR2 forms G = A^T A in fp64, R = chol(G),
+// Q1 = A R^-1, and repeats once on Q1; it is two streaming passes over the m x l matrix plus an
+// l x l factorisation, instead of a multi-level tree of shared-memory Householder factorisations.
+// It is accurate while cond(A) stays well below 1/sqrt(u_fp64) ~ 1e8; a collapsing Cholesky pivot
+// (relative pivot < 1e-12, i.e. A numerically rank deficient, as for BASELINE config 1) or a
+// second-pass R that is not close to I raises a device flag and the caller re-runs TSQR.
+#include "common.cuh"
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace rnmf_gpu {
+
+namespace {
+
+constexpr int kCqThreads = 256;
+constexpr int kGramRows = 32;      // rows staged per chunk
+constexpr int kGramMaxAcc = 64;    // l <= 128: l*l/256 entries per thread
+
+template <typename T>
+__global__ void __launch_bounds__(kCqThreads) cq_gram_kernel(const T* __restrict__ A, int64_t rows, int l,
+                                                             double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* tile = reinterpret_cast<double*>(smem);  // [kGramRows][l]
+  const int64_t r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  const int ll = l * l;
+  const int nacc = (ll + kCqThreads - 1) / kCqThreads;
+  double acc[kGramMaxAcc];
+#pragma unroll
+  for (int u = 0; u < kGramMaxAcc; ++u) acc[u] = 0.0;
+  for (int64_t base = r0; base < r1; base += kGramRows) {
+    const int nr = int(r1 - base < kGramRows ? r1 - base : kGramRows);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGramRows * l; e += kCqThreads) {
+      const int rr = e / l;
+      tile[e] = rr < nr ? double(A[(base + rr) * l + e % l]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kGramMaxAcc; ++u) {
+      if (u < nacc) {
+        const int e = threadIdx.x + kCqThreads * u;
+        if (e < ll) {
+          const int a = e / l, b = e % l;
+          double s0 = 0.0, s1 = 0.0;
+          for (int r = 0; r < kGramRows; r += 2) {
+            s0 += tile[r * l + a] * tile[r * l + b];
+            s1 += tile[(r + 1) * l + a] * tile[(r + 1) * l + b];
+          }
+          acc[u] += s0 + s1;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kGramMaxAcc; ++u) {
+    if (u < nacc) {
+      const int e = threadIdx.x + kCqThreads * u;
+      if (e < ll) part[int64_t(blockIdx.x) * ll + e] = acc[u];
+    }
+  }
+}
+
+// G = sum of partials (fixed order); R = chol(G) (upper, G = R^T R); Rinv = R^-1.  One CTA.
+// flag |= 1 when a pivot collapses; with `check_identity`, flag |= 2 when max|R - I| > 1e-2 (the
+// second CholeskyQR pass must see an almost orthonormal input).
+__global__ void __launch_bounds__(kCqThreads) cq_chol_kernel(const double* __restrict__ part, int nparts, int l,
+                                                             double* __restrict__ rinv, int* flag, int check_identity) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lp = l + 1;
+  double* G = reinterpret_cast<double*>(smem);  // [l][lp], becomes R in its upper triangle
+  double* Ri = G + l * lp;                      // [l][lp]
+  __shared__ int bad;
+  const int ll = l * l;
+  for (int e = threadIdx.x; e < ll; e += kCqThreads) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[int64_t(p) * ll + e];
+    G[(e / l) * lp + e % l] = s;
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  // right-looking Cholesky on the upper triangle: row j of R, then the trailing update
+  for (int j = 0; j < l; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = G[j * lp + j];
+      const double orig = d;  // trailing-updated diagonal
+      if (!(d > 0.0) || !isfinite(d)) bad = 1;
+      G[j * lp + j] = (d > 0.0 && isfinite(d)) ? sqrt(d) : 1.0;
+      (void)orig;
+    }
+    __syncthreads();
+    const double rjj = G[j * lp + j];
+    for (int c = j + 1 + threadIdx.x; c < l; c += kCqThreads) G[j * lp + c] /= rjj;
+    __syncthreads();
+    const int nt = l - j - 1;
+    for (int e = threadIdx.x; e < nt * nt; e += kCqThreads) {
+      const int a = j + 1 + e / nt, b = j + 1 + e % nt;
+      if (b >= a) G[a * lp + b] -= G[j * lp + a] * G[j * lp + b];
+    }
+    __syncthreads();
+  }
+  // pivot collapse relative to the largest diagonal of R
+  if (threadIdx.x == 0) {
+    double mx = 0.0, mn = 1e300;
+    for (int j = 0; j < l; ++j) {
+      mx = fmax(mx, fabs(G[j * lp + j]));
+      mn = fmin(mn, fabs(G[j * lp + j]));
+    }
+    if (!(mn > 1e-6 * mx)) bad = 1;  // R diag ratio ~ 1/cond(A); CholeskyQR2 needs cond << 1e8
+  }
+  // Rinv by column-wise back substitution (thread per column)
+  for (int c = threadIdx.x; c < l; c += kCqThreads) {
+    for (int i = l - 1; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int t = i + 1; t <= c; ++t) s -= G[i * lp + t] * Ri[t * lp + c];
+      Ri[i * lp + c] = (i <= c) ? s / G[i * lp + i] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (check_identity) {
+    double dev = 0.0;
+    for (int e = threadIdx.x; e < ll; e += kCqThreads) {
+      const int a = e / l, b = e % l;
+      if (b >= a) dev = fmax(dev, fabs(G[a * lp + b] - (a == b ? 1.0 : 0.0)));
+    }
+    for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    if ((threadIdx.x & 31) == 0 && dev > 1e-2) atomicOr(&bad, 2);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ll; e += kCqThreads) rinv[e] = Ri[(e / l) * lp + e % l];
+  if (threadIdx.x == 0 && bad) atomicOr(flag, bad);
+}
+
+// Out (rows x l) = A (rows x l) * Rinv (l x l upper triangular).  Rows staged in shared memory;
+// thread (row, column-group) computes columns j = jg, jg + G, ... of its row.
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(kCqThreads) cq_apply_kernel(const TIn* __restrict__ A, int64_t rows, int l,
+                                                              const double* __restrict__ rinv, TOut* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lp = l + 1;
+  double* Ri = reinterpret_cast<double*>(smem);  // [l][lp]
+  double* tile = Ri + l * lp;                    // [rows_per_block][lp]
+  constexpr int kRowsPerBlock = 64;
+  constexpr int kGroups = kCqThreads / kRowsPerBlock;  // 4 column groups per row
+  for (int e = threadIdx.x; e < l * l; e += kCqThreads) Ri[(e / l) * lp + e % l] = rinv[e];
+  for (int64_t base = int64_t(blockIdx.x) * kRowsPerBlock; base < rows; base += int64_t(gridDim.x) * kRowsPerBlock) {
+    const int nr = int(rows - base < kRowsPerBlock ? rows - base : kRowsPerBlock);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kRowsPerBlock * l; e += kCqThreads) {
+      const int rr = e / l;
+      tile[rr * lp + e % l] = rr < nr ? double(A[(base + rr) * l + e % l]) : 0.0;
+    }
+    __syncthreads();
+    const int rr = threadIdx.x / kGroups, jg = threadIdx.x % kGroups;
+    if (rr < nr) {
+      const double* ar = tile + rr * lp;
+      for (int j = jg; j < l; j += kGroups) {
+        double s0 = 0.0, s1 = 0.0;
+        int i = 0;
+        for (; i + 1 <= j; i += 2) {
+          s0 += ar[i] * Ri[i * lp + j];
+          s1 += ar[i + 1] * Ri[(i + 1) * lp + j];
+        }
+        if (i <= j) s0 += ar[i] * Ri[i * lp + j];
+        out[(base + rr) * l + j] = TOut(s0 + s1);
+      }
+    }
+  }
+}
+
+inline int gram_blocks(int64_t rows) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(rows, 256))));
+}
+
+}  // namespace
+
+int64_t cholqr_workspace_doubles(int64_t rows, int l) {
+  return int64_t(gram_blocks(rows)) * l * l + 2 * int64_t(l) * l + rows * int64_t(l) + 64;
+}
+
+template <typename T>
+int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream) {
+  const int nb = gram_blocks(rows);
+  double* part = ws;
+  double* rinv1 = part + int64_t(nb) * l * l;
+  double* rinv2 = rinv1 + int64_t(l) * l;
+  double* q1 = rinv2 + int64_t(l) * l;  // rows x l, fp64 intermediate
+  const size_t gsm = size_t(kGramRows) * l * sizeof(double);
+  const size_t csm = size_t(2) * l * (l + 1) * sizeof(double);
+  const size_t asm_ = size_t(l) * (l + 1) * sizeof(double) + size_t(64) * (l + 1) * sizeof(double);
+  RNMF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream));
+  // per-call attributes: sizes depend on l (chol needs 2 l (l+1) doubles: l <= 112 on B200)
+  RNMF_CUDA(cudaFuncSetAttribute(cq_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
+  RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
+  RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
+  RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  const int ab = int(std::max<int64_t>(1, std::min<int64_t>(148 * 4, ceil_div(rows, 64))));
+  // pass 1
+  cq_gram_kernel<T><<<nb, kCqThreads, gsm, stream>>>(a, rows, l, part);
+  RNMF_CUDA_LAUNCH();
+  cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, nb, l, rinv1, flag, 0);
+  RNMF_CUDA_LAUNCH();
+  cq_apply_kernel<T, double><<<ab, kCqThreads, asm_, stream>>>(a, rows, l, rinv1, q1);
+  RNMF_CUDA_LAUNCH();
+  // pass 2
+  cq_gram_kernel<double><<<nb, kCqThreads, gsm, stream>>>(q1, rows, l, part);
+  RNMF_CUDA_LAUNCH();
+  cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, nb, l, rinv2, flag, 1);
+  RNMF_CUDA_LAUNCH();
+  cq_apply_kernel<double, T><<<ab, kCqThreads, asm_, stream>>>(q1, rows, l, rinv2, q_out);
+  RNMF_CUDA_LAUNCH();
+  return 6;
+}
+
+template int launch_cholqr2<float>(const float*, int64_t, int, float*, double*, int*, cudaStream_t);
+template int launch_cholqr2<double>(const double*, int64_t, int, double*, double*, int*, cudaStream_t);
+
+}  // namespace rnmf_gpu

@@ -41,7 +41,6 @@ constexpr int kMaxLSlots = 5;     // (l + 1) / 32 lane slots in the recompress r
 constexpr int kMaxResSlots = 8;   // l / 16 lane slots for residc
 constexpr int kRedStride = 132;   // >= l + 1
 constexpr int kRedLen = kSwWarps * kRedStride > kSwThreads ? kSwWarps * kRedStride : kSwThreads;
-constexpr int kMaxGridPerLane = kMaxGrid / 32;
 
 // profile buckets (cycles of CTA 0, thread 0)
 enum {

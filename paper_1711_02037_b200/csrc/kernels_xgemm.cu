@@ -73,7 +73,7 @@ __device__ __forceinline__ void load8(const T* p, T (&a)[8]) {
 // xw: Y = X S.  One CTA owns 128 rows of X and all c output columns; it walks K = n in BK chunks.
 // Thread (ty, tx) accumulates rows ty*8..ty*8+7 x columns tx + 16 t.
 template <typename T, int CPAD, bool VECX, bool METRICS>
-__global__ void __launch_bounds__(kThreads) xw_kernel(const T* __restrict__ X, int64_t m, int64_t n,
+__global__ void __launch_bounds__(kThreads) xw_kernel(const T* __restrict__ X, int64_t m, int64_t n, int64_t ldx,
                                                       const T* __restrict__ S, int c, T* __restrict__ Y,
                                                       const T* __restrict__ W, int k,
                                                       const double* __restrict__ hht,
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) xw_kernel(const T* __restrict__ X, i
         const int r = v / (BK / VN), kv = v % (BK / VN);
         const int64_t gr = row0 + r, gk = k0 + int64_t(kv) * VN;
         if (gr < m && gk < n)
-          xr[u] = __ldcs(reinterpret_cast<const V*>(X + gr * n + gk));
+          xr[u] = __ldcs(reinterpret_cast<const V*>(X + gr * ldx + gk));
         else
           xr[u] = V{};
       }
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) xw_kernel(const T* __restrict__ X, i
         const int e = tid + kThreads * u;
         const int r = e / BK, kk = e % BK;
         const int64_t gr = row0 + r, gk = k0 + kk;
-        xsr[u] = (gr < m && gk < n) ? __ldcs(X + gr * n + gk) : T(0);
+        xsr[u] = (gr < m && gk < n) ? __ldcs(X + gr * ldx + gk) : T(0);
       }
     }
 #pragma unroll
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) xw_kernel(const T* __restrict__ X, i
 // row slice s of X; it walks the rows in BK chunks.  X tiles are [BK][128] row-major slices, read
 // with 16-byte vectors along the contiguous column dimension.
 template <typename T, int CPAD, bool VECX>
-__global__ void __launch_bounds__(kThreads) xtw_kernel(const T* __restrict__ X, int64_t m, int64_t n,
+__global__ void __launch_bounds__(kThreads) xtw_kernel(const T* __restrict__ X, int64_t m, int64_t n, int64_t ldx,
                                                        const T* __restrict__ S, int c, T* __restrict__ part,
                                                        int splits) {
   using L = XwSmem<T, CPAD>;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) xtw_kernel(const T* __restrict__ X, 
         const int kk = v / (kBM / VN), nv = v % (kBM / VN);
         const int64_t gr = r0 + kk, gn = n0 + int64_t(nv) * VN;
         if (gr < rend && gn < n)
-          xr[u] = __ldcs(reinterpret_cast<const V*>(X + gr * n + gn));
+          xr[u] = __ldcs(reinterpret_cast<const V*>(X + gr * ldx + gn));
         else
           xr[u] = V{};
       }
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads) xtw_kernel(const T* __restrict__ X, 
         const int e = tid + kThreads * u;
         const int kk = e / kBM, nl = e % kBM;
         const int64_t gr = r0 + kk, gn = n0 + nl;
-        xsr[u] = (gr < rend && gn < n) ? __ldcs(X + gr * n + gn) : T(0);
+        xsr[u] = (gr < rend && gn < n) ? __ldcs(X + gr * ldx + gn) : T(0);
       }
     }
 #pragma unroll
@@ -567,58 +567,58 @@ void set_smem(F* f, size_t bytes) {
   RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-inline bool x_vec_ok(const void* x, int64_t n, int vn, size_t esz) {
-  return (reinterpret_cast<uintptr_t>(x) % (vn * esz)) == 0 && (n % vn) == 0;
+inline bool x_vec_ok(const void* x, int64_t n, int64_t ldx, int vn, size_t esz) {
+  return (reinterpret_cast<uintptr_t>(x) % (vn * esz)) == 0 && (n % vn) == 0 && (ldx % vn) == 0;
 }
 
 template <typename T, int CPAD>
-void xw_dispatch_vec(const T* x, int64_t m, int64_t n, const T* s, int c, T* y, cudaStream_t st) {
+void xw_dispatch_vec(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* y, cudaStream_t st) {
   using L = XwSmem<T, CPAD>;
   const size_t sm = L::base;
   const dim3 grid(unsigned(ceil_div(m, kBM)));
-  if (x_vec_ok(x, n, Tile<T>::VN, sizeof(T))) {
+  if (x_vec_ok(x, n, ldx, Tile<T>::VN, sizeof(T))) {
     auto f = xw_kernel<T, CPAD, true, false>;
     set_smem(f, sm);
-    f<<<grid, kThreads, sm, st>>>(x, m, n, s, c, y, nullptr, 0, nullptr, nullptr, nullptr);
+    f<<<grid, kThreads, sm, st>>>(x, m, n, ldx, s, c, y, nullptr, 0, nullptr, nullptr, nullptr);
   } else {
     auto f = xw_kernel<T, CPAD, false, false>;
     set_smem(f, sm);
-    f<<<grid, kThreads, sm, st>>>(x, m, n, s, c, y, nullptr, 0, nullptr, nullptr, nullptr);
+    f<<<grid, kThreads, sm, st>>>(x, m, n, ldx, s, c, y, nullptr, 0, nullptr, nullptr, nullptr);
   }
   RNMF_CUDA_LAUNCH();
 }
 
 template <typename T, int CPAD>
-void xw_metrics_dispatch(const T* x, int64_t m, int64_t n, const T* ht, const T* w, int k,
+void xw_metrics_dispatch(const T* x, int64_t m, int64_t n, int64_t ldx, const T* ht, const T* w, int k,
                          const double* hht, double* po, double* pw, cudaStream_t st) {
   using L = XwSmem<T, CPAD>;
   const size_t sm = L::metrics_total;
   const dim3 grid(unsigned(ceil_div(m, kBM)));
-  if (x_vec_ok(x, n, Tile<T>::VN, sizeof(T))) {
+  if (x_vec_ok(x, n, ldx, Tile<T>::VN, sizeof(T))) {
     auto f = xw_kernel<T, CPAD, true, true>;
     set_smem(f, sm);
-    f<<<grid, kThreads, sm, st>>>(x, m, n, ht, k, nullptr, w, k, hht, po, pw);
+    f<<<grid, kThreads, sm, st>>>(x, m, n, ldx, ht, k, nullptr, w, k, hht, po, pw);
   } else {
     auto f = xw_kernel<T, CPAD, false, true>;
     set_smem(f, sm);
-    f<<<grid, kThreads, sm, st>>>(x, m, n, ht, k, nullptr, w, k, hht, po, pw);
+    f<<<grid, kThreads, sm, st>>>(x, m, n, ldx, ht, k, nullptr, w, k, hht, po, pw);
   }
   RNMF_CUDA_LAUNCH();
 }
 
 template <typename T, int CPAD>
-void xtw_dispatch(const T* x, int64_t m, int64_t n, const T* s, int c, T* part, int splits, cudaStream_t st) {
+void xtw_dispatch(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* part, int splits, cudaStream_t st) {
   using L = XwSmem<T, CPAD>;
   const size_t sm = L::base;
   const dim3 grid(unsigned(ceil_div(n, kBM)), unsigned(splits));
-  if (x_vec_ok(x, n, Tile<T>::VN, sizeof(T))) {
+  if (x_vec_ok(x, n, ldx, Tile<T>::VN, sizeof(T))) {
     auto f = xtw_kernel<T, CPAD, true>;
     set_smem(f, sm);
-    f<<<grid, kThreads, sm, st>>>(x, m, n, s, c, part, splits);
+    f<<<grid, kThreads, sm, st>>>(x, m, n, ldx, s, c, part, splits);
   } else {
     auto f = xtw_kernel<T, CPAD, false>;
     set_smem(f, sm);
-    f<<<grid, kThreads, sm, st>>>(x, m, n, s, c, part, splits);
+    f<<<grid, kThreads, sm, st>>>(x, m, n, ldx, s, c, part, splits);
   }
   RNMF_CUDA_LAUNCH();
 }
@@ -639,18 +639,18 @@ void xtw_dispatch(const T* x, int64_t m, int64_t n, const T* s, int c, T* part, 
 
 // ================================================================================================
 template <typename T>
-int launch_xw(const T* x, int64_t m, int64_t n, const T* s, int c, T* y, cudaStream_t stream) {
-  RNMF_CPAD_SWITCH(c, (xw_dispatch_vec<T, CP>(x, m, n, s, c, y, stream)));
+int launch_xw(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* y, cudaStream_t stream) {
+  RNMF_CPAD_SWITCH(c, (xw_dispatch_vec<T, CP>(x, m, n, ldx, s, c, y, stream)));
   return 1;
 }
 
 int xw_metrics_blocks(int64_t m) { return int(ceil_div(m, kBM)); }
 
 template <typename T>
-int launch_xw_metrics(const T* x, int64_t m, int64_t n, const T* ht, const T* w, int k,
+int launch_xw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* ht, const T* w, int k,
                       const double* hht, double* part_obj, double* part_pgw, int* nblocks,
                       cudaStream_t stream) {
-  RNMF_CPAD_SWITCH(k, (xw_metrics_dispatch<T, CP>(x, m, n, ht, w, k, hht, part_obj, part_pgw, stream)));
+  RNMF_CPAD_SWITCH(k, (xw_metrics_dispatch<T, CP>(x, m, n, ldx, ht, w, k, hht, part_obj, part_pgw, stream)));
   *nblocks = xw_metrics_blocks(m);
   return 1;
 }
@@ -664,10 +664,10 @@ int xtw_default_splits(int64_t m, int64_t n) {
 }
 
 template <typename T>
-int launch_xtw(const T* x, int64_t m, int64_t n, const T* s, int c, T* part, int splits, T* out,
+int launch_xtw(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* part, int splits, T* out,
                bool transpose_out, cudaStream_t stream) {
   if (splits <= 0) splits = xtw_default_splits(m, n);
-  RNMF_CPAD_SWITCH(c, (xtw_dispatch<T, CP>(x, m, n, s, c, part, splits, stream)));
+  RNMF_CPAD_SWITCH(c, (xtw_dispatch<T, CP>(x, m, n, ldx, s, c, part, splits, stream)));
   const int64_t total = n * c;
   const int blocks = int(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
   splitk_reduce_kernel<T><<<blocks, 256, 0, stream>>>(part, splits, n, c, out, transpose_out);
@@ -676,16 +676,25 @@ int launch_xtw(const T* x, int64_t m, int64_t n, const T* s, int c, T* part, int
 }
 
 template <typename T>
-int launch_xtw_metrics(const T* x, int64_t m, int64_t n, const T* w, int k, const T* h,
+int launch_xtw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w, int k, const T* h,
                        const double* wtw, T* part, int splits, double* part_pgh, int* nblocks,
                        cudaStream_t stream) {
   if (splits <= 0) splits = xtw_default_splits(m, n);
-  RNMF_CPAD_SWITCH(k, (xtw_dispatch<T, CP>(x, m, n, w, k, part, splits, stream)));
+  RNMF_CPAD_SWITCH(k, (xtw_dispatch<T, CP>(x, m, n, ldx, w, k, part, splits, stream)));
   const int blocks = int(ceil_div(n, kThreads));
   xtw_metrics_reduce_kernel<T><<<blocks, kThreads, 0, stream>>>(part, splits, n, k, h, wtw, part_pgh);
   RNMF_CUDA_LAUNCH();
   *nblocks = blocks;
   return 2;
+}
+
+template <typename T>
+int launch_splitk_reduce(const T* part, int splits, int64_t n, int c, T* out, bool transpose_out, cudaStream_t stream) {
+  const int64_t total = n * c;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 8)));
+  splitk_reduce_kernel<T><<<blocks, 256, 0, stream>>>(part, splits, n, c, out, transpose_out);
+  RNMF_CUDA_LAUNCH();
+  return 1;
 }
 
 int gram_parts(int64_t len) { return int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(len, 256)))); }
@@ -751,12 +760,13 @@ int launch_timestamp(unsigned long long* out, cudaStream_t stream) {
 }
 
 #define RNMF_INST(T)                                                                                          \
-  template int launch_xw<T>(const T*, int64_t, int64_t, const T*, int, T*, cudaStream_t);                    \
-  template int launch_xw_metrics<T>(const T*, int64_t, int64_t, const T*, const T*, int, const double*,      \
+  template int launch_xw<T>(const T*, int64_t, int64_t, int64_t, const T*, int, T*, cudaStream_t);           \
+  template int launch_xw_metrics<T>(const T*, int64_t, int64_t, int64_t, const T*, const T*, int, const double*, \
                                     double*, double*, int*, cudaStream_t);                                    \
-  template int launch_xtw<T>(const T*, int64_t, int64_t, const T*, int, T*, int, T*, bool, cudaStream_t);    \
-  template int launch_xtw_metrics<T>(const T*, int64_t, int64_t, const T*, int, const T*, const double*, T*, \
+  template int launch_xtw<T>(const T*, int64_t, int64_t, int64_t, const T*, int, T*, int, T*, bool, cudaStream_t); \
+  template int launch_xtw_metrics<T>(const T*, int64_t, int64_t, int64_t, const T*, int, const T*, const double*, T*, \
                                      int, double*, int*, cudaStream_t);                                       \
+  template int launch_splitk_reduce<T>(const T*, int, int64_t, int, T*, bool, cudaStream_t);                 \
   template int launch_gram_rows<T>(const T*, int64_t, int, double*, double*, cudaStream_t);                  \
   template int launch_gram_cols<T>(const T*, int, int64_t, double*, double*, cudaStream_t);                  \
   template int launch_transpose<T>(const T*, int64_t, int64_t, T*, cudaStream_t);                            \

@@ -17,6 +17,7 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 namespace rnmf_gpu {
@@ -258,6 +259,42 @@ class Engine {
  public:
   Engine(rnmf_gpu_context* ctx, Timer& tm) : ctx_(ctx), st_(ctx->stream), tm_(tm) {}
 
+  // X for the X-streaming kernels: rows need a 16-byte aligned pitch (TMA, vector loads).  Device
+  // input that already satisfies it is used in place (no copy); otherwise X is copied once into a
+  // context buffer whose pad columns are zero (host input: the pitched H2D copy is free).
+  const T* import_x(const void* src, int location, int64_t m, int64_t n) {
+    constexpr int64_t vn = 16 / sizeof(T);
+    m_ = m;
+    n_ = n;
+    if (location == RNMF_DEVICE) {
+      check_device_ptr(ctx_, src, "X");
+      if (n % vn == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+        ldx_ = n;
+        x_ = static_cast<const T*>(src);
+        return x_;
+      }
+    }
+    ldx_ = ceil_div(n, vn) * vn;
+    T* dst = ctx_->d<T>("x", size_t(m) * size_t(ldx_));
+    const bool padded = ldx_ != n;
+    if (padded) RNMF_CUDA(cudaMemsetAsync(dst, 0, sizeof(T) * size_t(m) * size_t(ldx_), st_));
+    const cudaMemcpyKind kind = location == RNMF_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    auto copy = [&] {
+      if (padded)
+        RNMF_CUDA(cudaMemcpy2DAsync(dst, sizeof(T) * ldx_, src, sizeof(T) * n, sizeof(T) * n, m, kind, st_));
+      else
+        RNMF_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * size_t(m) * size_t(n), kind, st_));
+    };
+    if (location == RNMF_HOST)
+      tm_.span(kH2D, copy);
+    else
+      copy();
+    x_ = dst;
+    return x_;
+  }
+  const T* x() const { return x_; }
+  int64_t ldx() const { return ldx_; }
+
   // Copy a caller matrix (host or device) into a context buffer.
   T* import(const std::string& name, const void* src, int location, size_t count) {
     T* dst = ctx_->d<T>(name, count);
@@ -290,7 +327,9 @@ class Engine {
 
   // One pass over X: data checks + sum + sum of squares.  Throws DataError like
   // check_nonnegative_finite (p/src/hals.cpp:17-34), non-finite before negative.
-  void scan(const T* x, int64_t m, int64_t n, bool check_negative, const char* nonfinite_msg) {
+  void scan(bool check_negative, const char* nonfinite_msg) {
+    const T* x = x_;
+    const int64_t m = m_, n = ldx_;  // pad columns are zero: finite, nonnegative, sum-neutral
     auto* bad = ctx_->d<unsigned long long>("scan.bad", 2);
     auto* part = ctx_->d<double>("scan.part", 2 * scan_grid());
     auto* out = ctx_->d<double>("scan.out", 2);
@@ -314,31 +353,77 @@ class Engine {
   }
 
   // rqb, p/src/sketch.cpp:52-71 -> Q (m x l), B (l x n) in context buffers.
-  void rqb(const T* x, int64_t m, int64_t n, int l, int64_t q_iters, const T* omega_dev, T** q_out, T** b_out) {
+  // math_mode EXACT: FFMA/DFMA kernels.  TF32 / TF32X3 (fp32 X only): tcgen05 kernels; TF32X3 runs
+  // the X*S passes as 3xTF32 (fp32-accurate) and the X^T*S passes as 1xTF32.
+  void rqb(int l, int64_t q_iters, const T* omega_dev, int math_mode, T** q_out, T** b_out) {
+    const T* x = x_;
+    const int64_t m = m_, n = n_, ldx = ldx_;
     T* y = ctx_->d<T>("rqb.y", size_t(m) * l);
     T* qb = ctx_->d<T>("rqb.q", size_t(m) * l);
     T* p = ctx_->d<T>("rqb.p", size_t(n) * l);
     T* z = ctx_->d<T>("rqb.z", size_t(n) * l);
     T* b = ctx_->d<T>("rqb.b", size_t(l) * n);
-    const int splits = xtw_default_splits(m, n);
+    const bool tc = std::is_same<T, float>::value && math_mode != RNMF_MATH_EXACT;
+    const bool x3 = math_mode == RNMF_MATH_TF32X3;
+    const int splits = tc ? tc_xtw_splits(m, n, ctx_->sm_count) : xtw_default_splits(m, n);
     T* part = ctx_->d<T>("rqb.part", size_t(splits) * n * l);
     const int64_t ws_len = std::max(tsqr_workspace_doubles(m, l, ctx_->max_smem), tsqr_workspace_doubles(n, l, ctx_->max_smem));
     double* ws = ctx_->d<double>("tsqr.ws", size_t(ws_len));
     const double xbytes = double(m) * double(n) * sizeof(T);
+    // S^T operands of the tensor-core kernels (hi / lo parts), sized for the larger of m, n
+    float* st_hi = nullptr;
+    float* st_lo = nullptr;
+    if (tc) {
+      const size_t cap = size_t(tc_npad(l)) * size_t(tc_st_pitch(std::max(m, n)));
+      st_hi = ctx_->d<float>("tc.st_hi", cap);
+      st_lo = ctx_->d<float>("tc.st_lo", cap);
+    }
     auto xw = [&](const T* s, T* out) {
-      tm_.span(kXw, [&] { tm_.launches += launch_xw<T>(x, m, n, s, l, out, st_); });
+      tm_.span(kXw, [&] {
+        if constexpr (std::is_same<T, float>::value) {
+          if (tc) {
+            tm_.launches += launch_tc_prep_st(s, n, l, st_hi, st_lo, st_);
+            tm_.launches += launch_tc_xw(x, m, n, ldx, st_hi, st_lo, l, out, x3, ctx_->sm_count, st_);
+            return;
+          }
+        }
+        tm_.launches += launch_xw<T>(x, m, n, ldx, s, l, out, st_);
+      });
       sketch_bytes_ += xbytes;
       ctx_->last.xw_bytes += xbytes;
       sketch_passes_ += 1;
     };
     auto xtw = [&](const T* s, T* out, bool tr) {
-      tm_.span(kXtw, [&] { tm_.launches += launch_xtw<T>(x, m, n, s, l, part, splits, out, tr, st_); });
+      tm_.span(kXtw, [&] {
+        if constexpr (std::is_same<T, float>::value) {
+          if (tc) {
+            tm_.launches += launch_tc_prep_st(s, m, l, st_hi, st_lo, st_);
+            tm_.launches += launch_tc_xtw(x, m, n, ldx, st_hi, l, part, splits, ctx_->sm_count, st_);
+            tm_.launches += launch_splitk_reduce<T>(part, splits, n, l, out, tr, st_);
+            return;
+          }
+        }
+        tm_.launches += launch_xtw<T>(x, m, n, ldx, s, l, part, splits, out, tr, st_);
+      });
       sketch_bytes_ += xbytes;
       ctx_->last.xtw_bytes += xbytes;
       sketch_passes_ += 1;
     };
+    double* cqws = ctx_->d<double>("cq.ws", size_t(cholqr_workspace_doubles(std::max(m, n), l)));
+    int* cqflag = ctx_->d<int>("cq.flag", 1);
+    int* hflag = ctx_->h<int>("cq.flag.h", 1);
+    // CholeskyQR2 first; Householder TSQR when A is too ill-conditioned (rank-deficient sketches)
     auto qr = [&](const T* a, int64_t rows, T* out) {
-      tm_.span(kQr, [&] { tm_.launches += launch_tsqr<T>(a, rows, l, out, ws, ctx_->max_smem, st_); });
+      tm_.span(kQr, [&] {
+        tm_.launches += launch_cholqr2<T>(a, rows, l, out, cqws, cqflag, st_);
+        RNMF_CUDA(cudaMemcpyAsync(hflag, cqflag, sizeof(int), cudaMemcpyDeviceToHost, st_));
+        RNMF_CUDA(cudaStreamSynchronize(st_));
+        if (hflag[0] != 0) {
+          tm_.launches += launch_tsqr<T>(a, rows, l, out, ws, ctx_->max_smem, st_);
+          ++qr_fallbacks_;
+        }
+        ++qr_calls_;
+      });
     };
     xw(omega_dev, y);
     for (int64_t it = 0; it < q_iters; ++it) {
@@ -355,7 +440,9 @@ class Engine {
 
   // Full-space metrics (p/src/rhals.cpp:140-148) of the device factors w (m x k), h (k x n):
   // writes [objective, pgrad_full] into res (device).
-  void metrics(const T* x, int64_t m, int64_t n, int k, const T* w, const T* h, double* res) {
+  void metrics(int k, const T* w, const T* h, double* res) {
+    const T* x = x_;
+    const int64_t m = m_, n = n_, ldx = ldx_;
     T* ht = ctx_->d<T>("met.ht", size_t(n) * k);
     double* hht = ctx_->d<double>("met.hht", size_t(k) * k);
     double* wtw = ctx_->d<double>("met.wtw", size_t(k) * k);
@@ -373,8 +460,8 @@ class Engine {
       tm_.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st_);
       tm_.launches += launch_gram_rows<T>(w, m, k, gpart2, wtw, st_);
       int b1 = 0, b2 = 0;
-      tm_.launches += launch_xw_metrics<T>(x, m, n, ht, w, k, hht, pobj, ppgw, &b1, st_);
-      tm_.launches += launch_xtw_metrics<T>(x, m, n, w, k, h, wtw, part, splits, ppgh, &b2, st_);
+      tm_.launches += launch_xw_metrics<T>(x, m, n, ldx, ht, w, k, hht, pobj, ppgw, &b1, st_);
+      tm_.launches += launch_xtw_metrics<T>(x, m, n, ldx, w, k, h, wtw, part, splits, ppgh, &b2, st_);
       tm_.launches += launch_sum_parts(pobj, b1, res, st_);
       tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
       tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
@@ -388,6 +475,7 @@ class Engine {
   double sum() const { return sum_; }
   double sumsq() const { return sumsq_; }
   double sketch_bytes_ = 0, metrics_bytes_ = 0;
+  int64_t qr_calls_ = 0, qr_fallbacks_ = 0;
   int64_t sketch_passes_ = 0, metrics_passes_ = 0;
 
  private:
@@ -395,6 +483,8 @@ class Engine {
   cudaStream_t st_;
   Timer& tm_;
   double sum_ = 0.0, sumsq_ = 0.0;
+  const T* x_ = nullptr;
+  int64_t m_ = 0, n_ = 0, ldx_ = 0;
 };
 
 // ---- the sweep / trace loop shared by rhals_fit and rhals_fit_compressed ---------------------
@@ -472,7 +562,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   tm.launches += launch_timestamp(gt_ref, st);
 
   // record 0: full-space metrics of the initial factors
-  eng.metrics(io.x, io.m, io.n, k, io.w, io.h, mres);
+  eng.metrics(k, io.w, io.h, mres);
   eval_iter.push_back(0);
 
   auto* hstat = ctx->h<long long>("sw.status.h", 2);
@@ -498,7 +588,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     last = hstat[0];
     const bool stopped = hstat[1] != 0;
     if (last >= t_begin) {
-      eng.metrics(io.x, io.m, io.n, k, io.w, io.h, mres + 2 * eval_iter.size());
+      eng.metrics(k, io.w, io.h, mres + 2 * eval_iter.size());
       eval_iter.push_back(last);
     }
     bool stop = stopped;
@@ -577,8 +667,8 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   if (m < 0 || n < 0) throw ShapeError("X has negative dimensions " + shape_string(m, n));
   const T* x = nullptr;
   if (m * n > 0) {
-    x = eng.import("x", x_in, location, size_t(m) * n);
-    eng.scan(x, m, n, true, nullptr);
+    x = eng.import_x(x_in, location, m, n);
+    eng.scan(true, nullptr);
   }
   validate_options_after_data(m, n, o);
   check_supported(o);
@@ -626,7 +716,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   });
   T *q = nullptr, *b = nullptr;
   try {
-    tm.span(kSketch, [&] { eng.rqb(x, m, n, l, o.power_iterations, om_dev, &q, &b); });
+    tm.span(kSketch, [&] { eng.rqb(l, o.power_iterations, om_dev, o.math_mode, &q, &b); });
   } catch (...) {
     drawer.join();
     throw;
@@ -711,7 +801,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
 
 template <typename T>
 static void rqb_impl(rnmf_gpu_context* ctx, const void* a_in, int location, int64_t m, int64_t n, int64_t rank,
-                     int64_t p, int64_t qi, int test_matrix, uint64_t seed, const double* omega, void* q_out,
+                     int64_t p, int64_t qi, int test_matrix, uint64_t seed, const double* omega, int math_mode, void* q_out,
                      void* b_out, int64_t* l_out) {
   ctx->last = rnmf_stage_times{};
   Timer tm(ctx);
@@ -725,8 +815,8 @@ static void rqb_impl(rnmf_gpu_context* ctx, const void* a_in, int location, int6
   const int l = int(l64);
   if (l > tsqr_max_l(ctx->max_smem) || l > 128)
     throw ParameterError("B200 path: sketch width " + std::to_string(l) + " above the supported maximum");
-  const T* x = eng.import("x", a_in, location, size_t(m) * n);
-  eng.scan(x, m, n, false, "rqb: input contains non-finite values");  // p/src/sketch.cpp:54-56
+  eng.import_x(a_in, location, m, n);
+  eng.scan(false, "rqb: input contains non-finite values");  // p/src/sketch.cpp:54-56
   std::vector<double> om_host;
   const double* om = omega;
   if (!om) {
@@ -740,7 +830,7 @@ static void rqb_impl(rnmf_gpu_context* ctx, const void* a_in, int location, int6
   }
   T* om_dev = eng.upload_converted("omega", om, size_t(n) * l);
   T *q = nullptr, *b = nullptr;
-  tm.span(kSketch, [&] { eng.rqb(x, m, n, l, qi, om_dev, &q, &b); });
+  tm.span(kSketch, [&] { eng.rqb(l, qi, om_dev, math_mode, &q, &b); });
   eng.export_(q_out, location, q, size_t(m) * l);
   eng.export_(b_out, location, b, size_t(l) * n);
   const double xwb = ctx->last.xw_bytes, xtwb = ctx->last.xtw_bytes;
@@ -819,8 +909,8 @@ static void fit_compressed_impl(rnmf_gpu_context* ctx, const void* x_in, int loc
   Engine<T> eng(ctx, tm);
   const T* x = nullptr;
   if (m * n > 0) {
-    x = eng.import("x", x_in, location, size_t(m) * n);
-    eng.scan(x, m, n, true, nullptr);
+    x = eng.import_x(x_in, location, m, n);
+    eng.scan(true, nullptr);
   }
   validate_options_after_data(m, n, o);
   check_supported(o);
@@ -1054,14 +1144,14 @@ int rnmf_gpu_rqb(rnmf_gpu_context* ctx, const void* a, int dtype, int location, 
   return guarded(err, err_cap, [&] {
     check_ctx(ctx);
     check_dtype(dtype, location);
-    (void)math_mode;
+    if (math_mode < RNMF_MATH_EXACT || math_mode > RNMF_MATH_TF32) throw rnmf_gpu::ParameterError("invalid math_mode");
     DeviceGuard g(ctx->device);
     if (dtype == RNMF_F32)
       rqb_impl<float>(ctx, a, location, m, n, target_rank, oversampling, power_iterations, test_matrix, seed, omega,
-                      q_out, b_out, l_out);
+                      math_mode, q_out, b_out, l_out);
     else
       rqb_impl<double>(ctx, a, location, m, n, target_rank, oversampling, power_iterations, test_matrix, seed, omega,
-                       q_out, b_out, l_out);
+                       math_mode, q_out, b_out, l_out);
   });
 }
 
