@@ -27,6 +27,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace rnmf_gpu {
 
@@ -99,7 +100,13 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
   return L;
 }
 
-template <typename T, bool QS>
+// LREG > 0 with QS: every CTA row slab has <= kSwThreads rows and l + 1 <= LREG <= 64; thread t keeps
+// Q row t in fp64 registers for the whole launch (lift = register dot product, recompress = warp
+// reduce-scatter), which removes the shared-memory round trips from the column chain.
+// LREG > 0 without QS (slab too large for shared memory, e.g. C3/C4): rows are streamed from L2 with
+// coalesced 16-byte loads, one row per thread per 256-row chunk; lift, clamp and the recompress
+// accumulation happen on the row while it is in registers (one pass over the slab per column).
+template <typename T, bool QS, int LREG>
 struct Sweeper {
   const SweepArgs<T>& a;
   int G, g, tid, lane, wid, l, k;
@@ -110,6 +117,7 @@ struct Sweeper {
   T *WsT, *Bc, *Hc, *Rc;
   unsigned epoch = 0;
   int slot = 0;
+  double qrow[(QS && LREG > 0) ? LREG : 1];
   // optional cycle profile of CTA 0 / thread 0 (args.prof != nullptr)
   bool prof_on = false;
   long long prof_last = 0;
@@ -179,6 +187,34 @@ struct Sweeper {
       return a.w[(r0 + r) * k + j];
   }
   __device__ __forceinline__ double wcol_get(int64_t r) const { return wcold[r]; }
+  // Row r of this CTA's Q slab into registers (streamed path).  fp32 Q: 16-byte vector loads when
+  // the row pitch allows.  Out-of-range rows / columns read as 0.
+  template <typename F>
+  __device__ __forceinline__ void load_row(int64_t r, F (&qf)[LREG > 0 ? LREG : 1]) const {
+    if (r >= R) {
+#pragma unroll
+      for (int i = 0; i < (LREG > 0 ? LREG : 1); ++i) qf[i] = F(0);
+      return;
+    }
+    const T* qr = a.q + (r0 + r) * l;
+    if constexpr (sizeof(T) == 4 && LREG > 0) {
+      if ((l % 4) == 0) {
+#pragma unroll
+        for (int i4 = 0; i4 < LREG / 4; ++i4) {
+          if (i4 * 4 < l) {
+            const float4 v4 = __ldg(reinterpret_cast<const float4*>(qr) + i4);
+            qf[4 * i4] = v4.x, qf[4 * i4 + 1] = v4.y, qf[4 * i4 + 2] = v4.z, qf[4 * i4 + 3] = v4.w;
+          } else {
+            qf[4 * i4] = qf[4 * i4 + 1] = qf[4 * i4 + 2] = qf[4 * i4 + 3] = F(0);
+          }
+        }
+        return;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < (LREG > 0 ? LREG : 1); ++i) qf[i] = i < l ? F(__ldg(qr + i)) : F(0);
+  }
+
   __device__ __forceinline__ double* part_base() { return a.part + int64_t(slot) * part_slot_len; }
   __device__ __forceinline__ double* fin_base() { return a.fin + int64_t(slot) * fin_slot_len; }
   __device__ __forceinline__ void next_slot() { slot ^= 1; }
@@ -201,15 +237,15 @@ struct Sweeper {
       double acc = 0.0;
       if (sidx < S) {
         const double* src = p + e0 + eb + el;
-        for (int gb = sidx; gb < G; gb += 16 * S) {
-          double v[16];
+        for (int gb = sidx; gb < G; gb += 32 * S) {
+          double v[32];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
+          for (int u = 0; u < 32; ++u) {
             const int gg = gb + u * S;
             v[u] = gg < G ? ld_cg(src + int64_t(gg) * L) : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 16; ++u) acc += v[u];
+          for (int u = 0; u < 32; ++u) acc += v[u];
         }
       }
       red[tid] = acc;
@@ -313,6 +349,10 @@ struct Sweeper {
       for (int e = tid; e < k * k; e += kSwThreads) Vm[e] = a.vm[e];
     }
     __syncthreads();
+    if constexpr (QS && LREG > 0) {
+#pragma unroll
+      for (int i = 0; i < LREG; ++i) qrow[i] = (tid < R && i < l) ? Qs[int64_t(tid) * lq + i] : 0.0;
+    }
   }
 
   __device__ void store_back(int64_t last, int stopped) {
@@ -350,19 +390,68 @@ struct Sweeper {
   __device__ void init_wt_wn() {
     const int lk = l * k, L = lk + k;
     double* p = part_base();
-    for (int e = tid; e < L; e += kSwThreads) {
-      double s = 0.0;
-      if (e < lk) {
-        const int i = e / k, j = e % k;
-        for (int64_t r = 0; r < R; ++r) s += q(r, i) * double(w_get(r, j));
-      } else {
-        const int j = e - lk;
-        for (int64_t r = 0; r < R; ++r) {
-          const double wv = double(w_get(r, j));
-          s += wv * wv;
+    if constexpr (QS) {
+      for (int e = tid; e < L; e += kSwThreads) {
+        double s = 0.0;
+        if (e < lk) {
+          const int i = e / k, j = e % k;
+          for (int64_t r = 0; r < R; ++r) s += q(r, i) * double(w_get(r, j));
+        } else {
+          const int j = e - lk;
+          for (int64_t r = 0; r < R; ++r) {
+            const double wv = double(w_get(r, j));
+            s += wv * wv;
+          }
+        }
+        p[int64_t(g) * L + e] = s;
+      }
+    } else {
+      // rows staged 4 at a time through shared memory (the red scratch is free here); entry blocks
+      // of 8 per thread, one pass over the slab per block
+      constexpr int kChunk = 4;
+      double* qst = red;                 // [kChunk][l]   (<= 512 doubles)
+      double* wst = red + kChunk * 128;  // [kChunk][k]   (<= 256 doubles)
+      for (int eb = 0; eb < L; eb += kSwThreads * 8) {
+        double accs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) accs[u] = 0.0;
+        for (int64_t base = 0; base < R; base += kChunk) {
+          const int nr = int(R - base < kChunk ? R - base : kChunk);
+          __syncthreads();
+          for (int e = tid; e < kChunk * l; e += kSwThreads) {
+            const int rr = e / l;
+            qst[e] = rr < nr ? double(a.q[(r0 + base + rr) * l + e % l]) : 0.0;
+          }
+          for (int e = tid; e < kChunk * k; e += kSwThreads) {
+            const int rr = e / k;
+            wst[e] = rr < nr ? double(a.w[(r0 + base + rr) * k + e % k]) : 0.0;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = eb + tid + kSwThreads * u;
+            if (e < L) {
+              double sacc = 0.0;
+              if (e < lk) {
+                const int i = e / k, jj = e % k;
+#pragma unroll
+                for (int rr = 0; rr < kChunk; ++rr) sacc += qst[rr * l + i] * wst[rr * k + jj];
+              } else {
+                const int jj = e - lk;
+#pragma unroll
+                for (int rr = 0; rr < kChunk; ++rr) sacc += wst[rr * k + jj] * wst[rr * k + jj];
+              }
+              accs[u] += sacc;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = eb + tid + kSwThreads * u;
+          if (e < L) p[int64_t(g) * L + e] = accs[u];
         }
       }
-      p[int64_t(g) * L + e] = s;
+      __syncthreads();
     }
     const bool do_wt = a.flags & kInitWt, do_wn = a.flags & kInitWn;
     allreduce2(L, [&](int e, double v) {
@@ -406,6 +495,122 @@ struct Sweeper {
     __syncthreads();
     prof_tick(kPfWStep);
     const double shift = beta != 0.0 ? beta / denom : 0.0;
+    const int L1 = l + 1;
+    if constexpr (QS && LREG > 0) {
+      // lift: thread t owns row t (register-resident Q row)
+      double wd = 0.0;
+      if (tid < R) {
+        double u[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < LREG; ++i)
+          if (i < l) u[i & 3] += qrow[i] * colnew[i];
+        double uu = (u[0] + u[1]) + (u[2] + u[3]);
+        if (beta != 0.0) uu -= shift;
+        wd = fmax(uu, 0.0);
+        wcold[tid] = wd;
+        if constexpr (QS)
+          WsT[int64_t(j) * RM + tid] = T(wd);
+        else
+          a.w[(r0 + tid) * k + j] = T(wd);
+      }
+      prof_tick(kPfLift);
+      // recompress partial: v_i = Q(t,i) w_t (i < l), v_l = w_t^2; warp reduce-scatter over the 32
+      // rows of the warp (lane L ends with entry L of each 32-entry chunk), then cross-warp in order
+#pragma unroll
+      for (int chunk = 0; chunk < (LREG + 31) / 32; ++chunk) {
+        if (chunk * 32 < L1) {
+          auto val = [&](int i) -> double {  // entry i of this thread's contribution vector
+            return (i < l) ? qrow[i < LREG ? i : 0] * wd : (i == l ? wd * wd : 0.0);
+          };
+          double v[16];
+          {
+            const bool hi = (lane & 16) != 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int ia = chunk * 32 + e, ib = ia + 16;
+              const double va = (ia < LREG || ia == l) ? val(ia) : 0.0;
+              const double vb = (ib < LREG || ib == l) ? val(ib) : 0.0;
+              const double send = hi ? va : vb;
+              const double mine = hi ? vb : va;
+              v[e] = mine + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+          }
+#pragma unroll
+          for (int off = 8; off >= 1; off >>= 1) {
+            const bool hi = (lane & off) != 0;
+#pragma unroll
+            for (int e = 0; e < off; ++e) {
+              const double send = hi ? v[e] : v[e + off];
+              const double mine = hi ? v[e + off] : v[e];
+              v[e] = mine + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+          const int i = chunk * 32 + lane;
+          if (i < L1) red[wid * kRedStride + i] = v[0];
+        }
+      }
+    } else if constexpr (LREG > 0) {
+      // streamed rows (Q slab not resident): one pass, row in registers, fp64 accumulators
+      double acc[LREG];
+#pragma unroll
+      for (int i = 0; i < LREG; ++i) acc[i] = 0.0;
+      // UNR rows per thread per iteration, all their loads issued before any is used
+      constexpr int UNR = (sizeof(T) == 4 && LREG <= 32) ? 4 : 1;
+      for (int64_t rb = tid; rb < R; rb += int64_t(kSwThreads) * UNR) {
+        T qf[UNR][LREG];
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int64_t r = rb + int64_t(kSwThreads) * uu;
+          load_row(r, qf[uu]);
+        }
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int64_t r = rb + int64_t(kSwThreads) * uu;
+          if (r >= R) continue;
+          double u[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < LREG; ++i)
+            if (i < l) u[i & 3] += double(qf[uu][i]) * colnew[i];
+          double uu2 = (u[0] + u[1]) + (u[2] + u[3]);
+          if (beta != 0.0) uu2 -= shift;
+          const double wd = fmax(uu2, 0.0);
+          a.w[(r0 + r) * k + j] = T(wd);
+#pragma unroll
+          for (int i = 0; i < LREG; ++i) acc[i] += (i < l ? double(qf[uu][i]) : (i == l ? wd : 0.0)) * wd;
+        }
+      }
+      prof_tick(kPfLift);
+#pragma unroll
+      for (int chunk = 0; chunk < (LREG + 31) / 32; ++chunk) {
+        if (chunk * 32 < L1) {
+          double v[16];
+          {
+            const bool hi = (lane & 16) != 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int ia = chunk * 32 + e, ib = ia + 16;
+              const double va = ia < LREG ? acc[ia < LREG ? ia : 0] : 0.0;
+              const double vb = ib < LREG ? acc[ib < LREG ? ib : 0] : 0.0;
+              const double send = hi ? va : vb;
+              const double mine = hi ? vb : va;
+              v[e] = mine + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+          }
+#pragma unroll
+          for (int off = 8; off >= 1; off >>= 1) {
+            const bool hi = (lane & off) != 0;
+#pragma unroll
+            for (int e = 0; e < off; ++e) {
+              const double send = hi ? v[e] : v[e + off];
+              const double mine = hi ? v[e + off] : v[e];
+              v[e] = mine + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+          const int i = chunk * 32 + lane;
+          if (i < L1) red[wid * kRedStride + i] = v[0];
+        }
+      }
+    } else {
     for (int64_t r = tid; r < R; r += kSwThreads) {
       double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
       int i = 0;
@@ -431,7 +636,6 @@ struct Sweeper {
     // (two interleaved accumulators); lane slot u covers output i = lane + 32 u, where output l
     // is the squared norm ("column l of Q" is W(:,j) itself).  Branch-free: inactive lanes
     // multiply by zero.
-    const int L1 = l + 1;
     {
       const int nslots = (L1 + 31) / 32;
       double a0[kMaxLSlots], a1[kMaxLSlots];
@@ -470,6 +674,7 @@ struct Sweeper {
         const int i = lane + 32 * u;
         if (u < nslots && i < L1) red[wid * kRedStride + i] = a0[u] + a1[u];
       }
+    }
     }
     __syncthreads();
     if (tid < L1) {
@@ -700,6 +905,47 @@ struct Sweeper {
   // Thread per row, 16 independent accumulators per pass (throughput- not latency-bound).
   __device__ double pgrad_w() {
     double acc = 0.0;
+    if constexpr (!QS && LREG > 0) {
+      constexpr int UNR = (sizeof(T) == 4 && LREG <= 32) ? 4 : 1;
+      for (int64_t rb = tid; rb < R; rb += int64_t(kSwThreads) * UNR) {
+        T qf[UNR][LREG];
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) load_row(rb + int64_t(kSwThreads) * uu, qf[uu]);
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int64_t r = rb + int64_t(kSwThreads) * uu;
+          if (r >= R) continue;
+          const T* wr = a.w + (r0 + r) * k;
+          for (int j0 = 0; j0 < k; j0 += 8) {
+            double sacc[8];
+            T wv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              sacc[t] = 0.0;
+              wv[t] = j0 + t < k ? wr[j0 + t] : T(0);
+            }
+#pragma unroll
+            for (int i = 0; i < LREG; ++i) {
+              if (i < l) {
+                const double qv = double(qf[uu][i]);
+                const double* ei = Em + i * kp + j0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                  if (j0 + t < k) sacc[t] += qv * ei[t];
+              }
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (j0 + t < k) {
+                const double gv = -2.0 * sacc[t];
+                const double gp = wv[t] > T(0) ? gv : fmin(0.0, gv);
+                acc += gp * gp;
+              }
+            }
+          }
+        }
+      }
+    } else
     for (int64_t r = tid; r < R; r += kSwThreads) {
       for (int j0 = 0; j0 < k; j0 += 16) {
         double sacc[16];
@@ -792,11 +1038,11 @@ struct Sweeper {
   }
 };
 
-template <typename T, bool QS>
+template <typename T, bool QS, int LREG>
 __global__ void __launch_bounds__(kSwThreads, 1) rhals_sweeps_kernel(SweepArgs<T> args, SmemLayout L, int64_t RM,
                                                                       int64_t NCM) {
   extern __shared__ __align__(16) unsigned char smem[];
-  Sweeper<T, QS> s(args, smem, L, RM, NCM);
+  Sweeper<T, QS, LREG> s(args, smem, L, RM, NCM);
   s.run();
 }
 
@@ -809,12 +1055,17 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
   const int G = sm_count;
   p.rows_per_cta = ceil_div(m, G);
   p.cols_per_cta = ceil_div(n, G);
-  for (int qs = 1; qs >= 0; --qs) {
+  // RNMF_FORCE_NOQS / RNMF_NO_QREG / RNMF_NO_QSTREAM: testing knobs that force the other code paths
+  for (int qs = std::getenv("RNMF_FORCE_NOQS") ? 0 : 1; qs >= 0; --qs) {
     const SmemLayout L = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, qs != 0);
     if (L.total <= size_t(max_smem)) {
       p.q_in_smem = qs != 0;
       p.smem = L.total;
       p.grid = G;
+      if (p.q_in_smem && p.rows_per_cta <= kSwThreads && l + 1 <= 64 && !std::getenv("RNMF_NO_QREG"))
+        p.lreg = (l + 1 <= 32) ? 32 : (l + 1 <= 48) ? 48 : 64;
+      if (!p.q_in_smem && !std::getenv("RNMF_NO_QSTREAM") && (l + 1 <= 32 || (sizeof(T) == 4 && l + 1 <= 64)))
+        p.lreg = (l + 1 <= 32) ? 32 : 64;
       return p;
     }
   }
@@ -829,8 +1080,15 @@ int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t 
   SweepArgs<T> a = args;
   int64_t RM = plan.rows_per_cta, NCM = plan.cols_per_cta;
   void* kargs[] = {&a, const_cast<SmemLayout*>(&L), &RM, &NCM};
-  const void* fn = plan.q_in_smem ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true>)
-                                  : reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false>);
+  const void* stream64 = nullptr;
+  if constexpr (sizeof(T) == 4) stream64 = reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 64>);
+  const void* fn = !plan.q_in_smem ? (plan.lreg == 32   ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 32>)
+                                      : plan.lreg == 64 ? stream64
+                                                        : reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 0>))
+                   : plan.lreg == 32 ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true, 32>)
+                   : plan.lreg == 48 ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true, 48>)
+                   : plan.lreg == 64 ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true, 64>)
+                                     : reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true, 0>);
   RNMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(plan.smem)));
   int occ = 0;
   RNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kSwThreads, plan.smem));

@@ -231,3 +231,20 @@ def test_stage_shape_errors(gpu):
         gpu.rhals_update_W(cp)
     with pytest.raises(gpu.ShapeError):
         gpu.rhals_update_H(cp)
+
+
+@pytest.mark.parametrize("knobs", [{"RNMF_NO_QREG": "1"}, {"RNMF_FORCE_NOQS": "1"},
+                                   {"RNMF_FORCE_NOQS": "1", "RNMF_NO_QSTREAM": "1"}])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_sweep_kernel_paths(gpu, oracle, knobs, dtype, monkeypatch):
+    """The persistent kernel's Q-slab paths (register-resident rows, shared-memory rows, rows
+    streamed from L2, generic) all reproduce the oracle."""
+    for kk, v in knobs.items():
+        monkeypatch.setenv(kk, v)
+    x = oracle.synth_lowrank(700, 260, 5, 0.1, 23)
+    o = _opts(gpu, rank=5, max_iter=25, tol=1e-300, oversampling=7, seed=2, reg=gpu.RegConfig(0.1, 0.2, 0.01, 0.02))
+    om, w0, h0 = workloads.injected_inputs(4, 700, 260, 5, 12)
+    ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    res = gpu.rhals_fit(x.astype(dtype), o, omega=om, w0=w0, h0=h0)
+    rtol = F64_TRACE_RTOL if dtype == np.float64 else F32_TRACE_RTOL
+    assert_trace_close(res.trace, ref.trace, rtol, F32_FINAL_ATOL)
