@@ -49,6 +49,20 @@ int launch_xtw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w
                        const double* wtw, T* part, int splits, double* part_pgh, int* nblocks,
                        cudaStream_t stream);
 
+// grad_H projected norm from W^T X split partials part[s][n][k] (fixed-order sum over s)
+template <typename T>
+int launch_grad_h_reduce(const T* part, int splits, int64_t n, int k, const T* h, const double* wtw, double* part_pgh,
+                         int* nblocks, cudaStream_t stream);
+
+// ---- fused one-pass metrics (kernels_metrics.cu): objective from the explicit residual, projected
+// grad_W, and (when wtx_part != nullptr) per-CTA partials of W^T X (metrics_grid(m) x n x k).
+int metrics_tiles(int64_t m);
+int metrics_grid(int64_t m, int sm_count);
+template <typename T>
+int launch_metrics_fused(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w, const T* h, int k,
+                         const double* hht, T* wtx_part, double* part_obj, double* part_pgw, int sm_count,
+                         cudaStream_t stream);
+
 // ---- small dense helpers (kernels_xgemm.cu) ---------------------------------------------------
 // G (c x c, fp64) = A^T A for A (rows x c) row-major.  part: gram_parts(rows)*c*c doubles.
 template <typename T>
@@ -83,8 +97,8 @@ int launch_tc_xw(const float* x, int64_t m, int64_t n, int64_t ldx, const float*
 // part[split] (n x c) = X[rows of split]^T S[rows of split]; S^T given as st (tc_npad(c) x
 // tc_st_pitch(m), K-major).  The caller reduces the splits.
 int tc_xtw_splits(int64_t m, int64_t n, int sm_count);
-int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, int c, float* part, int splits,
-                  int sm_count, cudaStream_t stream);
+int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int c,
+                  float* part, int splits, bool x3, int sm_count, cudaStream_t stream);
 
 // ---- tall-skinny QR (kernels_tsqr.cu) ---------------------------------------------------------
 // Householder TSQR of A (rows x l, row-major) -> explicit thin Q (rows x l, written to q_out in

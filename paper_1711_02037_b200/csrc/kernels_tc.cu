@@ -206,11 +206,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xw_kernel(const __grid_const
 //       K = 32 X rows per stage (SBO = 1024 B per 8 rows)
 //   B = S^T slab (N = NPAD rows of the transposed small operand, K-major)
 // One work unit = (128-column tile, row split); units are distributed over persistent CTAs.
-template <int NPAD>
+template <int NPAD, bool X3 = false>
 struct XtwCfg {
   static constexpr int kXBytes = 128 * kBK * 4;  // 32 rows x 128 cols
   static constexpr int kSBytes = NPAD * kBK * 4;
-  static constexpr int kStageBytes = kXBytes + kSBytes;
+  static constexpr int kStageBytes = (kXBytes + kSBytes) * (X3 ? 2 : 1);
   static constexpr int kStages = std::min(6, (200 * 1024) / kStageBytes);
   static constexpr int kTmemCols = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64) ? 64 : (2 * NPAD <= 128) ? 128 : 256;
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
@@ -223,21 +223,25 @@ struct XtwParams {
   float* part;  // splits x n x c
 };
 
-template <int NPAD>
+template <int NPAD, bool X3>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_constant__ CUtensorMap tmX,
-                                                               const __grid_constant__ CUtensorMap tmSt, XtwParams p) {
-  using C = XtwCfg<NPAD>;
+                                                               const __grid_constant__ CUtensorMap tmSt,
+                                                               const __grid_constant__ CUtensorMap tmStLo, XtwParams p) {
+  using C = XtwCfg<NPAD, X3>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto xs = [&](int s) { return smem + size_t(s) * C::kStageBytes; };
   auto ss = [&](int s) { return smem + size_t(s) * C::kStageBytes + C::kXBytes; };
+  auto xl = [&](int s) { return smem + size_t(s) * C::kStageBytes + C::kXBytes + C::kSBytes; };
+  auto sl = [&](int s) { return xl(s) + C::kXBytes; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::kStageBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
   uint64_t* tempty = bars + 2 * S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  uint64_t* split = bars + 2 * S + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ctiles = ceil_div(p.n, 128);
@@ -247,6 +251,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&split[s], 64);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmX);
     tc::tma_prefetch(&tmSt);
+    if (X3) tc::tma_prefetch(&tmStLo);
   }
   if (warp == 1) tc::tmem_alloc<C::kTmemCols>(tmem_slot);
   tc::tc_fence_before();
@@ -280,10 +286,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
         for (int64_t r = r0; r < r1; r += kBK, ++it) {
           const int s = int(it % S);
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kXBytes + C::kSBytes));
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kXBytes + C::kSBytes * (X3 ? 2 : 1)));
 #pragma unroll
           for (int b = 0; b < 4; ++b) tc::tma_load_2d(xs(s) + b * 4096, &tmX, &full[s], int(ct * 128 + b * 32), int(r));
           tc::tma_load_2d(ss(s), &tmSt, &full[s], int(r), 0);
+          if (X3) tc::tma_load_2d(sl(s), &tmStLo, &full[s], int(r), 0);
         }
       }
     }
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
       bool first = true;
       for (int64_t r = r0; r < r1; r += kBK, ++it) {
         const int s = int(it % S);
-        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(X3 ? &split[s] : &full[s], (it / S) & 1);
         tc::tc_fence_after();
         if (tc::elect_one()) {
           const uint32_t xa = tc::smem_u32(xs(s)), ba = tc::smem_u32(ss(s));
@@ -310,6 +317,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
             const uint64_t adesc = tc::make_sdesc(xa + k * 1024, 4096, 512, tc::kLayoutSW128Base32B);
             const uint64_t bdesc = tc::make_sdesc(ba + k * 32, 16, 1024);
             tc::umma_tf32(d, adesc, bdesc, idesc, (first && k == 0) ? 0u : 1u);
+            if (X3) {
+              const uint64_t al = tc::make_sdesc(tc::smem_u32(xl(s)) + k * 1024, 4096, 512, tc::kLayoutSW128Base32B);
+              const uint64_t bl = tc::make_sdesc(tc::smem_u32(sl(s)) + k * 32, 16, 1024);
+              tc::umma_tf32(d, adesc, bl, idesc, 1);
+              tc::umma_tf32(d, al, bdesc, idesc, 1);
+            }
           }
           tc::umma_commit(&empty[s]);
           if (r + kBK >= r1) tc::umma_commit(&tfull[acc]);
@@ -322,7 +335,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    if (X3) {  // 3xTF32 split of the X tile (elementwise, so the swizzled layout is irrelevant)
+      const int st = threadIdx.x - 64;
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t r0, r1;
+        unit_rows(u, r0, r1);
+        for (int64_t r = r0; r < r1; r += kBK, ++it) {
+          const int s = int(it % S);
+          tc::mbar_wait(&full[s], (it / S) & 1);
+          float4* x4 = reinterpret_cast<float4*>(xs(s));
+          float4* l4 = reinterpret_cast<float4*>(xl(s));
+#pragma unroll 4
+          for (int q = st; q < C::kXBytes / 16; q += 64) {
+            float4 v = x4[q], lo;
+            float h;
+            h = tc::tf32_hi(v.x), lo.x = v.x - h, v.x = h;
+            h = tc::tf32_hi(v.y), lo.y = v.y - h, v.y = h;
+            h = tc::tf32_hi(v.z), lo.z = v.z - h, v.z = h;
+            h = tc::tf32_hi(v.w), lo.w = v.w - h, v.w = h;
+            x4[q] = v;
+            l4[q] = lo;
+          }
+          tc::fence_proxy_async_smem();
+          tc::mbar_arrive(&split[s]);
+        }
+      }
+    }
+  } else {
     const int sub = warp & 3;
     uint32_t ti = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ti) {
@@ -425,18 +466,19 @@ void tc_xw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float
 }
 
 
-template <int NPAD>
-void tc_xtw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, int64_t ldst, int c, float* part,
-                   int splits, int sm_count, cudaStream_t stream) {
-  using C = XtwCfg<NPAD>;
+template <int NPAD, bool X3>
+void tc_xtw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int64_t ldst,
+                   int c, float* part, int splits, int sm_count, cudaStream_t stream) {
+  using C = XtwCfg<NPAD, X3>;
   const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);  // 32 x 32 boxes
   const CUtensorMap ms = make_map_2d(st, NPAD, m, ldst, NPAD);  // S^T: NPAD rows x m
+  const CUtensorMap ml = make_map_2d(X3 ? st_lo : st, NPAD, m, ldst, NPAD);
   XtwParams p{m, n, c, splits, part};
-  auto f = tc_xtw_kernel<NPAD>;
+  auto f = tc_xtw_kernel<NPAD, X3>;
   RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
   const int64_t units = ceil_div(n, 128) * splits;
   const int grid = int(std::min<int64_t>(units, sm_count));
-  f<<<grid, kTcThreads, C::kSmem, stream>>>(mx, ms, p);
+  f<<<grid, kTcThreads, C::kSmem, stream>>>(mx, ms, ml, p);
   RNMF_CUDA_LAUNCH();
 }
 
@@ -449,20 +491,20 @@ int tc_xtw_splits(int64_t m, int64_t n, int sm_count) {
   return int(s);
 }
 
-int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, int c, float* part, int splits,
-                  int sm_count, cudaStream_t stream) {
+int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int c,
+                  float* part, int splits, bool x3, int sm_count, cudaStream_t stream) {
   if ((ldx * sizeof(float)) % 16 != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0)
     throw CudaError("tc_xtw: X needs a 16-byte aligned base and row pitch");
   const int64_t ldst = tc_st_pitch(m);
   switch (tc_npad(c)) {
-    case 16: tc_xtw_launch<16>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 32: tc_xtw_launch<32>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 48: tc_xtw_launch<48>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 64: tc_xtw_launch<64>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 80: tc_xtw_launch<80>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 96: tc_xtw_launch<96>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 112: tc_xtw_launch<112>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
-    case 128: tc_xtw_launch<128>(x, m, n, ldx, st, ldst, c, part, splits, sm_count, stream); break;
+    case 16: if (x3) tc_xtw_launch<16, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<16, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 32: if (x3) tc_xtw_launch<32, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<32, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 48: if (x3) tc_xtw_launch<48, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<48, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 64: if (x3) tc_xtw_launch<64, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<64, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 80: if (x3) tc_xtw_launch<80, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<80, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 96: if (x3) tc_xtw_launch<96, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<96, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 112: if (x3) tc_xtw_launch<112, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<112, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
+    case 128: if (x3) tc_xtw_launch<128, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); else tc_xtw_launch<128, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream); break;
     default: throw CudaError("tc_xtw: column count above 128");
   }
   return 1;

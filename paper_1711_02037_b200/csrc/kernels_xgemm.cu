@@ -413,28 +413,35 @@ __global__ void splitk_reduce_kernel(const T* __restrict__ part, int splits, int
   }
 }
 
-// Metrics pass 2 epilogue: per X column `col`, grad_H(:,col) = -2 (W^T X(:,col) - (W^T W) H(:,col)),
-// projected by H(:,col), squared and summed; one partial per CTA.
+// Metrics grad_H epilogue: for each (X column col, j), sum the split partials of (W^T X)(j, col) in
+// fixed order, form grad_H(j, col) = -2 ((W^T X)(j, col) - ((W^T W) H)(j, col)), project by
+// H(j, col), square; one partial sum per CTA.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) xtw_metrics_reduce_kernel(const T* __restrict__ part, int splits,
                                                                       int64_t n, int k,
                                                                       const T* __restrict__ H,
                                                                       const double* __restrict__ wtw,
                                                                       double* part_pgh) {
-  const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // e = col * k + j
   double acc = 0.0;
-  if (col < n) {
+  if (e < n * k) {
+    const int64_t col = e / k;
+    const int j = int(e % k);
     const int64_t total = n * k;
-    for (int j = 0; j < k; ++j) {
-      double a = 0.0;
-      for (int s = 0; s < splits; ++s) a += double(part[int64_t(s) * total + col * k + j]);
-      double b = 0.0;
-      for (int t = 0; t < k; ++t) b += wtw[j * k + t] * double(H[int64_t(t) * n + col]);
-      const double g = -2.0 * (a - b);
-      const double hv = double(H[int64_t(j) * n + col]);
-      const double gp = hv > 0.0 ? g : fmin(g, 0.0);
-      acc += gp * gp;
+    double a0 = 0.0, a1 = 0.0;
+    int s = 0;
+    for (; s + 1 < splits; s += 2) {
+      a0 += double(part[int64_t(s) * total + e]);
+      a1 += double(part[int64_t(s + 1) * total + e]);
     }
+    if (s < splits) a0 += double(part[int64_t(s) * total + e]);
+    const double a = a0 + a1;
+    double b = 0.0;
+    for (int t = 0; t < k; ++t) b += wtw[j * k + t] * double(H[int64_t(t) * n + col]);
+    const double g = -2.0 * (a - b);
+    const double hv = double(H[int64_t(j) * n + col]);
+    const double gp = hv > 0.0 ? g : fmin(g, 0.0);
+    acc = gp * gp;
   }
   __shared__ double red[kThreads / 32];
   acc = warp_allreduce_sum(acc);
@@ -681,11 +688,20 @@ int launch_xtw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w
                        cudaStream_t stream) {
   if (splits <= 0) splits = xtw_default_splits(m, n);
   RNMF_CPAD_SWITCH(k, (xtw_dispatch<T, CP>(x, m, n, ldx, w, k, part, splits, stream)));
-  const int blocks = int(ceil_div(n, kThreads));
+  int b = 0;
+  launch_grad_h_reduce<T>(part, splits, n, k, h, wtw, part_pgh, &b, stream);
+  *nblocks = b;
+  return 2;
+}
+
+template <typename T>
+int launch_grad_h_reduce(const T* part, int splits, int64_t n, int k, const T* h, const double* wtw, double* part_pgh,
+                         int* nblocks, cudaStream_t stream) {
+  const int blocks = int(ceil_div(n * k, kThreads));
   xtw_metrics_reduce_kernel<T><<<blocks, kThreads, 0, stream>>>(part, splits, n, k, h, wtw, part_pgh);
   RNMF_CUDA_LAUNCH();
   *nblocks = blocks;
-  return 2;
+  return 1;
 }
 
 template <typename T>
@@ -767,6 +783,8 @@ int launch_timestamp(unsigned long long* out, cudaStream_t stream) {
   template int launch_xtw_metrics<T>(const T*, int64_t, int64_t, int64_t, const T*, int, const T*, const double*, T*, \
                                      int, double*, int*, cudaStream_t);                                       \
   template int launch_splitk_reduce<T>(const T*, int, int64_t, int, T*, bool, cudaStream_t);                 \
+  template int launch_grad_h_reduce<T>(const T*, int, int64_t, int, const T*, const double*, double*, int*,   \
+                                       cudaStream_t);                                                         \
   template int launch_gram_rows<T>(const T*, int64_t, int, double*, double*, cudaStream_t);                  \
   template int launch_gram_cols<T>(const T*, int, int64_t, double*, double*, cudaStream_t);                  \
   template int launch_transpose<T>(const T*, int64_t, int64_t, T*, cudaStream_t);                            \

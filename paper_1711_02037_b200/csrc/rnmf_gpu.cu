@@ -354,7 +354,7 @@ class Engine {
 
   // rqb, p/src/sketch.cpp:52-71 -> Q (m x l), B (l x n) in context buffers.
   // math_mode EXACT: FFMA/DFMA kernels.  TF32 / TF32X3 (fp32 X only): tcgen05 kernels; TF32X3 runs
-  // the X*S passes as 3xTF32 (fp32-accurate) and the X^T*S passes as 1xTF32.
+  // every X pass as 3xTF32 (hi/lo split of both operands, fp32-accurate).
   void rqb(int l, int64_t q_iters, const T* omega_dev, int math_mode, T** q_out, T** b_out) {
     const T* x = x_;
     const int64_t m = m_, n = n_, ldx = ldx_;
@@ -398,7 +398,7 @@ class Engine {
         if constexpr (std::is_same<T, float>::value) {
           if (tc) {
             tm_.launches += launch_tc_prep_st(s, m, l, st_hi, st_lo, st_);
-            tm_.launches += launch_tc_xtw(x, m, n, ldx, st_hi, l, part, splits, ctx_->sm_count, st_);
+            tm_.launches += launch_tc_xtw(x, m, n, ldx, st_hi, st_lo, l, part, splits, x3, ctx_->sm_count, st_);
             tm_.launches += launch_splitk_reduce<T>(part, splits, n, l, out, tr, st_);
             return;
           }
@@ -453,23 +453,50 @@ class Engine {
     double* ppgw = ctx_->d<double>("met.ppgw", size_t(nb1));
     const int splits = xtw_default_splits(m, n);
     T* part = ctx_->d<T>("met.part", size_t(splits) * n * k);
-    double* ppgh = ctx_->d<double>("met.ppgh", size_t(ceil_div(n, 256)));
+    double* ppgh = ctx_->d<double>("met.ppgh", size_t(ceil_div(n * k, 256)));
     double* tmp = ctx_->d<double>("met.tmp", 4);
+    // one fused X pass when the per-tile W^T X partials stay small (<= 1/4 of X), else the fused
+    // pass without W^T X plus a split-K X^T W pass
+    const bool fused_ok = k <= 64 && (sizeof(T) == 4 || k <= 32);
+    const double wtx_bytes = double(metrics_grid(m, ctx_->sm_count)) * double(n) * k * sizeof(T);
+    const bool one_pass = fused_ok && wtx_bytes <= 0.25 * double(m) * double(n) * sizeof(T);
+    x_passes_ = 2;
     tm_.span(kMetrics, [&] {
-      tm_.launches += launch_transpose<T>(h, k, n, ht, st_);
       tm_.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st_);
       tm_.launches += launch_gram_rows<T>(w, m, k, gpart2, wtw, st_);
       int b1 = 0, b2 = 0;
-      tm_.launches += launch_xw_metrics<T>(x, m, n, ldx, ht, w, k, hht, pobj, ppgw, &b1, st_);
-      tm_.launches += launch_xtw_metrics<T>(x, m, n, ldx, w, k, h, wtw, part, splits, ppgh, &b2, st_);
+      if (fused_ok) {
+        T* wtx = one_pass ? ctx_->d<T>("met.wtx", size_t(metrics_grid(m, ctx_->sm_count)) * n * k) : nullptr;
+        const int g1 = metrics_grid(m, ctx_->sm_count);
+        double* po = ctx_->d<double>("met.pobj2", size_t(g1));
+        double* pw = ctx_->d<double>("met.ppgw2", size_t(g1));
+        tm_.launches += launch_metrics_fused<T>(x, m, n, ldx, w, h, k, hht, wtx, po, pw, ctx_->sm_count, st_);
+        b1 = g1;
+        pobj = po;
+        ppgw = pw;
+        if (one_pass) {
+          double* pgh = ctx_->d<double>("met.ppgh2", size_t(ceil_div(n * k, 256)));
+          tm_.launches += launch_grad_h_reduce<T>(wtx, metrics_grid(m, ctx_->sm_count), n, k, h, wtw, pgh, &b2, st_);
+          ppgh = pgh;
+          x_passes_ = 1;
+        } else {
+          double* pgh = ctx_->d<double>("met.ppgh2", size_t(ceil_div(n * k, 256)));
+          tm_.launches += launch_xtw_metrics<T>(x, m, n, ldx, w, k, h, wtw, part, splits, pgh, &b2, st_);
+          ppgh = pgh;
+        }
+      } else {
+        tm_.launches += launch_transpose<T>(h, k, n, ht, st_);
+        tm_.launches += launch_xw_metrics<T>(x, m, n, ldx, ht, w, k, hht, pobj, ppgw, &b1, st_);
+        tm_.launches += launch_xtw_metrics<T>(x, m, n, ldx, w, k, h, wtw, part, splits, ppgh, &b2, st_);
+      }
       tm_.launches += launch_sum_parts(pobj, b1, res, st_);
       tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
       tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
       // res[1] = pgw + pgh, done on device by a 2-element sum
       tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
     });
-    metrics_bytes_ += 2.0 * double(m) * double(n) * sizeof(T);
-    metrics_passes_ += 2;
+    metrics_bytes_ += double(x_passes_) * double(m) * double(n) * sizeof(T);
+    metrics_passes_ += x_passes_;
   }
 
   double sum() const { return sum_; }
@@ -485,6 +512,7 @@ class Engine {
   double sum_ = 0.0, sumsq_ = 0.0;
   const T* x_ = nullptr;
   int64_t m_ = 0, n_ = 0, ldx_ = 0;
+  int x_passes_ = 2;
 };
 
 // ---- the sweep / trace loop shared by rhals_fit and rhals_fit_compressed ---------------------

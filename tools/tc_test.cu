@@ -109,7 +109,8 @@ int xtw_main(int64_t m, int64_t n, int c, int reps) {
   CK(cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ds, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
   launch_tc_prep_st(ds, m, c, dh, dl, 0);
-  launch_tc_xtw(dx, m, n, ldx, dh, c, dp, splits, prop.multiProcessorCount, 0);
+  for (int x3 = 0; x3 < 2; ++x3) {
+  launch_tc_xtw(dx, m, n, ldx, dh, dl, c, dp, splits, x3, prop.multiProcessorCount, 0);
   CK(cudaDeviceSynchronize());
   std::vector<float> part(size_t(splits) * n * c);
   CK(cudaMemcpy(part.data(), dp, part.size() * 4, cudaMemcpyDeviceToHost));
@@ -129,14 +130,15 @@ int xtw_main(int64_t m, int64_t n, int c, int reps) {
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   CK(cudaEventRecord(a));
-  for (int r = 0; r < reps; ++r) launch_tc_xtw(dx, m, n, ldx, dh, c, dp, splits, prop.multiProcessorCount, 0);
+  for (int r = 0; r < reps; ++r) launch_tc_xtw(dx, m, n, ldx, dh, dl, c, dp, splits, x3, prop.multiProcessorCount, 0);
   CK(cudaEventRecord(b));
   CK(cudaEventSynchronize(b));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, a, b));
   ms /= reps;
-  std::printf("tc_xtw m=%lld n=%lld c=%d splits=%d: max |err|/sum|terms| = %.3e  %.4f ms  %.0f GB/s\n", (long long)m,
-              (long long)n, c, splits, maxrel, ms, double(m) * n * 4 / (ms * 1e-3) / 1e9);
+  std::printf("tc_xtw m=%lld n=%lld c=%d splits=%d x3=%d: max |err|/sum|terms| = %.3e  %.4f ms  %.0f GB/s\n",
+              (long long)m, (long long)n, c, splits, x3, maxrel, ms, double(m) * n * 4 / (ms * 1e-3) / 1e9);
+  }
   return 0;
 }
 
