@@ -7,7 +7,8 @@ import os
 from ._abi import ProblemShapeC, RegConfigC, SolverOptionsC, StageTimesC, TraceRecordC
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "librnmf_gpu.so")
+# RNMF_GPU_LIB: development override (e.g. a build with the sweep-kernel cycle profile compiled in)
+LIB_PATH = os.environ.get("RNMF_GPU_LIB") or os.path.join(HERE, "lib", "librnmf_gpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "rnmf_gpu.h")
 
 _lib = None

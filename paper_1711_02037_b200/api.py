@@ -355,8 +355,10 @@ def compress(x, opts: SolverOptions, *, omega=None, w0=None, h0=None, ctx: Optio
     return CompressedProblem(q, b, wt, w, h)
 
 
-def rqb(a, opts: SketchOptions, *, omega=None, ctx: Optional[Context] = None) -> SketchResult:
-    """rnmf::rqb (p/src/sketch.cpp:52-71) on the GPU."""
+def rqb(a, opts: SketchOptions, *, omega=None, ctx: Optional[Context] = None,
+        math_mode: int = MathMode.Exact) -> SketchResult:
+    """rnmf::rqb (p/src/sketch.cpp:52-71) on the GPU.  `math_mode` selects the arithmetic of the
+    X-streaming GEMMs (MathMode; Exact = FMA in the working precision)."""
     A = _Mat(a, name="A")
     m, n = A.shape
     c = _ctx_for(A.device or 0, ctx)
@@ -376,7 +378,7 @@ def rqb(a, opts: SketchOptions, *, omega=None, ctx: Optional[Context] = None) ->
     _sync_torch(A)
     st = lib().rnmf_gpu_rqb(c.handle, A.ptr, A.dtype_code, A.location, m, n, int(opts.target_rank),
                             int(opts.oversampling), int(opts.power_iterations), int(opts.test_matrix),
-                            ctypes.c_uint64(int(opts.seed) & 0xFFFFFFFFFFFFFFFF), _dptr(om), 0, _ptr(q), _ptr(b),
+                            ctypes.c_uint64(int(opts.seed) & 0xFFFFFFFFFFFFFFFF), _dptr(om), int(math_mode), _ptr(q), _ptr(b),
                             ctypes.byref(lo), e, _CAP)
     raise_for_status(st, e)
     return SketchResult(q, b)

@@ -155,7 +155,8 @@ struct SweepArgs {
   double* fin;             // [2 * sweep_part_len(l,k)]
   long long* prof;         // optional: per-phase cycle counters of CTA 0 (kSweepProfSlots)
 };
-constexpr int kSweepProfSlots = 14;  // 13 buckets + barrier count
+bool sweep_prof_compiled();  // built with RNMF_SWEEP_PROF=1
+constexpr int kSweepProfSlots = 17;  // 16 buckets + barrier count
 
 __host__ __device__ inline int64_t sweep_part_len(int l, int k) {
   const int64_t a = 2 * int64_t(l) * k + int64_t(k) * k + 2;

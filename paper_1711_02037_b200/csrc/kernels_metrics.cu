@@ -24,7 +24,6 @@ constexpr int kMBN = 32;   // columns per chunk
 
 template <typename T, int KP>
 struct MetCfg {
-  static constexpr int kXS = 0;                 // (no transposed copy)
   static constexpr int kXR = kMBN + 4;          // Xr[r][c] row stride (keeps 16 B alignment)
   static constexpr int kWS = kMBM + 4;          // WsT[j][r]
   static constexpr int kWR = KP + 4;            // Wr[r][j]

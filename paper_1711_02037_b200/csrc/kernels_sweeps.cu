@@ -37,16 +37,19 @@ constexpr int kSwThreads = 256;
 constexpr int kSwWarps = kSwThreads / 32;
 constexpr int kMaxPerLane = 4;  // k, l <= 128
 constexpr double kDivisionFloor = 1e-12;  // p/include/rnmf/hals.hpp:67
-constexpr int kMaxGrid = 256;
 constexpr int kMaxLSlots = 5;     // (l + 1) / 32 lane slots in the recompress reduction
 constexpr int kMaxResSlots = 8;   // l / 16 lane slots for residc
 constexpr int kRedStride = 132;   // >= l + 1
 constexpr int kRedLen = kSwWarps * kRedStride > kSwThreads ? kSwWarps * kRedStride : kSwThreads;
 
+#ifndef RNMF_SWEEP_PROF
+#define RNMF_SWEEP_PROF 0
+#endif
+constexpr bool kSweepProf = RNMF_SWEEP_PROF != 0;
 // profile buckets (cycles of CTA 0, thread 0)
 enum {
   kPfWStep, kPfLift, kPfRecomp, kPfBarrier1, kPfReduce1, kPfHCols, kPfHProducts, kPfBarrier2, kPfReduce2a,
-  kPfReduce2b, kPfPgw, kPfOther, kPfSweeps, kPfCount
+  kPfReduce2b, kPfPgw, kPfOther, kPfHS, kPfHInit, kPfHUpd, kPfSweeps, kPfCount
 };
 
 struct SmemLayout {
@@ -118,12 +121,13 @@ struct Sweeper {
   unsigned epoch = 0;
   int slot = 0;
   double qrow[(QS && LREG > 0) ? LREG : 1];
-  // optional cycle profile of CTA 0 / thread 0 (args.prof != nullptr)
+  // optional cycle profile of CTA 0 / thread 0 (built with RNMF_SWEEP_PROF=1 and args.prof != nullptr;
+  // compiled out otherwise, the runtime test alone costs a reconvergence point per tick)
   bool prof_on = false;
   long long prof_last = 0;
   long long prof_acc[kPfCount] = {};
   __device__ __forceinline__ void prof_tick(int bucket) {
-    if (prof_on) {
+    if (kSweepProf && prof_on) {
       const long long now = clock64();
       prof_acc[bucket] += now - prof_last;
       prof_last = now;
@@ -170,7 +174,7 @@ struct Sweeper {
     Rc = reinterpret_cast<T*>(smem + L.rc);
     part_slot_len = sweep_part_len(l, k) * G;
     fin_slot_len = sweep_part_len(l, k);
-    prof_on = a.prof != nullptr && g == 0 && tid == 0;
+    prof_on = kSweepProf && a.prof != nullptr && g == 0 && tid == 0;
     if (prof_on) prof_last = clock64();
   }
 
@@ -722,8 +726,14 @@ struct Sweeper {
   __device__ void h_phase(bool update, bool grad_valid, double& objc, double& pgh) {
     prof_tick(kPfOther);
     compute_s();
+    prof_tick(kPfHS);
     const double alpha = a.alpha_h, beta = a.beta_h;
-    const int LPC = k <= 16 ? 16 : 32;
+    int LPC = k <= 16 ? 16 : 32;
+    // narrower column groups when the CTA owns more columns than one round of LPC-lane groups
+    // covers (e.g. 17 columns at LPC 16 would take two full rounds while the grid waits)
+    while (LPC > 4 && NC > int64_t(kSwWarps) * (32 / LPC) && (k + LPC / 2 - 1) / (LPC / 2) <= kMaxPerLane &&
+           (l + LPC / 2 - 1) / (LPC / 2) <= kMaxResSlots)
+      LPC /= 2;
     const int CPW = 32 / LPC;
     const int sub = lane / LPC, sl = lane % LPC;
     double objc_l = 0.0, pgh_l = 0.0;
@@ -748,43 +758,41 @@ struct Sweeper {
         r[t] = r0v + r1v;
         acc[t] = 0.0;
       }
+      prof_tick(kPfHInit);
       // acc_j = sum_i S(i, j) h_i
-      for (int i = 0; i < k; ++i) {
-        double src = 0.0;
+      // (the source slot ts is a compile-time index: register arrays stay in registers)
 #pragma unroll
-        for (int t = 0; t < kMaxPerLane; ++t)
-          if (t == i / LPC) src = h[t];
-        const double hi = __shfl_sync(0xffffffffu, src, i % LPC, LPC);
+      for (int ts = 0; ts < kMaxPerLane; ++ts) {
+        for (int o = 0; o < LPC && ts * LPC + o < k; ++o) {
+          const int i = ts * LPC + o;
+          const double hi = __shfl_sync(0xffffffffu, h[ts], o, LPC);
 #pragma unroll
-        for (int t = 0; t < kMaxPerLane; ++t) {
-          const int j = sl + LPC * t;
-          if (j < k) acc[t] += Sm[i * k + j] * hi;
+          for (int t = 0; t < kMaxPerLane; ++t) {
+            const int j = sl + LPC * t;
+            if (j < k) acc[t] += Sm[i * k + j] * hi;
+          }
         }
       }
       if (update) {
-        for (int j = 0; j < k; ++j) {
-          const int owner = j % LPC, slot = j / LPC;
-          double delta = 0.0;
-          if (sl == owner) {
+#pragma unroll
+        for (int ts = 0; ts < kMaxPerLane; ++ts) {
+          for (int owner = 0; owner < LPC && ts * LPC + owner < k; ++owner) {
+            const int j = ts * LPC + owner;
+            // branch-free: every lane evaluates its own candidate, the owner's is broadcast
+            double num = r[ts] - acc[ts] - alpha * h[ts];
+            if (beta != 0.0) num -= beta;
+            const double hn = fmax(0.0, h[ts] + num * invd[j]);
+            const double dj = __shfl_sync(0xffffffffu, hn - h[ts], owner, LPC);
+            if (sl == owner) h[ts] = hn;
 #pragma unroll
             for (int t = 0; t < kMaxPerLane; ++t) {
-              if (t == slot) {
-                double num = r[t] - acc[t] - alpha * h[t];
-                if (beta != 0.0) num -= beta;
-                const double hn = fmax(0.0, h[t] + num * invd[j]);
-                delta = hn - h[t];
-                h[t] = hn;
-              }
+              const int jj = sl + LPC * t;
+              if (jj < k) acc[t] += Sm[j * k + jj] * dj;
             }
-          }
-          const double dj = __shfl_sync(0xffffffffu, delta, owner, LPC);
-#pragma unroll
-          for (int t = 0; t < kMaxPerLane; ++t) {
-            const int jj = sl + LPC * t;
-            if (jj < k) acc[t] += Sm[j * k + jj] * dj;
           }
         }
       }
+      prof_tick(kPfHUpd);
       // residc(:,c) = B(:,c) - W~ h
       double res[kMaxResSlots];
 #pragma unroll
@@ -792,16 +800,16 @@ struct Sweeper {
         const int i = sl + LPC * u;
         res[u] = (i < l) ? double(Bc[i * ncp + clx]) : 0.0;
       }
-      for (int j = 0; j < k; ++j) {
-        double src = 0.0;
 #pragma unroll
-        for (int t = 0; t < kMaxPerLane; ++t)
-          if (t == j / LPC) src = h[t];
-        const double hj = __shfl_sync(0xffffffffu, src, j % LPC, LPC);
+      for (int ts = 0; ts < kMaxPerLane; ++ts) {
+        for (int o = 0; o < LPC && ts * LPC + o < k; ++o) {
+          const int j = ts * LPC + o;
+          const double hj = __shfl_sync(0xffffffffu, h[ts], o, LPC);
 #pragma unroll
-        for (int u = 0; u < kMaxResSlots; ++u) {
-          const int i = sl + LPC * u;
-          if (i < l) res[u] -= Wt[i * kp + j] * hj;
+          for (int u = 0; u < kMaxResSlots; ++u) {
+            const int i = sl + LPC * u;
+            if (i < l) res[u] -= Wt[i * kp + j] * hj;
+          }
         }
       }
       double gs[kMaxPerLane];
@@ -809,16 +817,16 @@ struct Sweeper {
       for (int t = 0; t < kMaxPerLane; ++t) gs[t] = 0.0;
       if (!grad_valid) {
         // -2 W~^T residc: broadcast residc entries across the column's lanes
-        for (int i = 0; i < l; ++i) {
-          double src = 0.0;
 #pragma unroll
-          for (int u = 0; u < kMaxResSlots; ++u)
-            if (u == i / LPC) src = res[u];
-          const double ri = __shfl_sync(0xffffffffu, src, i % LPC, LPC);
+        for (int us = 0; us < kMaxResSlots; ++us) {
+          for (int o = 0; o < LPC && us * LPC + o < l; ++o) {
+            const int i = us * LPC + o;
+            const double ri = __shfl_sync(0xffffffffu, res[us], o, LPC);
 #pragma unroll
-          for (int t = 0; t < kMaxPerLane; ++t) {
-            const int jj = sl + LPC * t;
-            if (jj < k) gs[t] += Wt[i * kp + jj] * ri;
+            for (int t = 0; t < kMaxPerLane; ++t) {
+              const int jj = sl + LPC * t;
+              if (jj < k) gs[t] += Wt[i * kp + jj] * ri;
+            }
           }
         }
       }
@@ -1029,7 +1037,7 @@ struct Sweeper {
         last = t;
       }
     }
-    if (prof_on) {
+    if (kSweepProf && prof_on) {
       prof_acc[kPfSweeps] = clock64() - t_start;
       for (int b = 0; b < kPfCount; ++b) a.prof[b] = prof_acc[b];
       a.prof[kPfCount] = epoch;
@@ -1101,5 +1109,7 @@ template SweepPlan plan_sweeps<float>(int64_t, int64_t, int, int, int, int);
 template SweepPlan plan_sweeps<double>(int64_t, int64_t, int, int, int, int);
 template int launch_sweeps<float>(const SweepArgs<float>&, const SweepPlan&, cudaStream_t);
 template int launch_sweeps<double>(const SweepArgs<double>&, const SweepPlan&, cudaStream_t);
+
+bool sweep_prof_compiled() { return kSweepProf; }
 
 }  // namespace rnmf_gpu

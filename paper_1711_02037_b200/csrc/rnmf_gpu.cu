@@ -570,7 +570,9 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
   // RNMF_PROF=1: per-phase cycle counters of CTA 0, printed to stderr (development aid)
-  const bool prof = std::getenv("RNMF_PROF") != nullptr;
+  const bool prof = std::getenv("RNMF_PROF") != nullptr && sweep_prof_compiled();
+  if (std::getenv("RNMF_PROF") != nullptr && !prof)
+    std::fprintf(stderr, "[rnmf prof] library built without RNMF_SWEEP_PROF=1; no cycle profile\n");
   std::vector<long long> prof_sum(kSweepProfSlots, 0);
   long long* hprof = nullptr;
   if (prof) {
@@ -664,7 +666,8 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   for (int64_t t = 1; t < nrec; ++t) trace[t].elapsed_s = std::max(trace[t].elapsed_s, trace[t - 1].elapsed_s);
   if (prof) {
     static const char* names[] = {"w_step", "lift", "recompress", "barrier1", "reduce1", "h_cols", "h_products",
-                                  "barrier2", "reduce2a", "reduce2b", "pgw", "other", "kernel_total", "barriers"};
+                                  "barrier2", "reduce2a", "reduce2b", "pgw", "other", "h_s", "h_init", "h_update",
+                                  "kernel_total", "barriers"};
     std::fprintf(stderr, "[rnmf prof] sweeps=%lld grid=%d smem=%zu q_in_smem=%d (cycles of CTA 0 summed over launches)\n",
                  (long long)last, plan.grid, plan.smem, int(plan.q_in_smem));
     for (int i = 0; i < kSweepProfSlots; ++i)

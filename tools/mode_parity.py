@@ -52,7 +52,9 @@ def main():
         for f in ("rel_err", "objective_compressed", "objective", "pgrad", "pgrad_full"):
             g = np.array([getattr(r, f) for r in res.trace])
             o = np.array([r[f] for r in ref.trace])
-            dev[f] = float(np.max(np.abs(g - o) / np.maximum(np.abs(o), 1e-300)))
+            rel = np.abs(g - o) / np.maximum(np.abs(o), 1e-300)
+            dev[f] = float(np.max(rel))
+            dev[f + "_worst_record"] = int(np.argmax(rel))
         out["modes"][mode.name] = {
             "max_rel_dev": dev,
             "final_rel_err_abs_diff": abs(res.trace[-1].rel_err - ref.trace[-1]["rel_err"]),
@@ -61,6 +63,25 @@ def main():
             "qr_ms": st["qr_ms"], "sweeps_ms": st["sweeps_ms"], "metrics_ms": st["metrics_ms"],
         }
     out["oracle_final_rel_err"] = ref.trace[-1]["rel_err"]
+    # sketch quality per mode: principal angles between range(Q_gpu) and range(Q_oracle), and the
+    # relative projection residual ||X - Q Q^T X|| / ||X||
+    l = omega.shape[1]
+    so = api.SketchOptions(target_rank=opts.rank, oversampling=opts.oversampling,
+                           power_iterations=opts.power_iterations)
+    qo, _ = orc.rqb(x.astype(np.float64), opts.rank, opts.oversampling, opts.power_iterations, omega=omega)
+    x64 = x.astype(np.float64)
+    nx = np.linalg.norm(x64)
+    out["sketch"] = {"oracle_proj_resid": float(np.linalg.norm(x64 - qo @ (qo.T @ x64)) / nx)}
+    for mode in (api.MathMode.Exact, api.MathMode.TF32x3, api.MathMode.TF32):
+        sk = api.rqb(xd, so, omega=omega, ctx=ctx, math_mode=mode)
+        q = sk.q.double().cpu().numpy() if hasattr(sk.q, "cpu") else np.asarray(sk.q, dtype=np.float64)
+        sv = np.linalg.svd(q.T @ qo, compute_uv=False)
+        sines = np.sqrt(np.maximum(0.0, 1.0 - np.clip(sv, 0, 1) ** 2))
+        out["sketch"][mode.name] = {
+            "sin_angles_top5": sorted(sines.tolist())[-5:],
+            "proj_resid": float(np.linalg.norm(x64 - q @ (q.T @ x64)) / nx),
+            "orth_err": float(np.linalg.norm(q.T @ q - np.eye(l))),
+        }
     print(json.dumps(out, indent=1))
 
 
