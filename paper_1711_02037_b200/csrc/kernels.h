@@ -125,7 +125,15 @@ enum SweepFlags : int {
   kDoW = 16,      // W phase in each sweep
   kDoH = 32,      // H phase (+ evaluation) in each sweep
   kRecord = 64,   // write trace entries / stop checks
+  kColOrdered = 128,  // column-step reduction through ordered fp64 partials (else fixed-point atomics)
 };
+// Sync block of the sweep kernel (zeroed before every launch): the grid-barrier counter at byte 0,
+// then a 3-slot ring of 64-bit fixed-point accumulators for the column step.
+constexpr int kColAccMax = 136;      // entries per slot, >= l + 1
+constexpr int kColAccSpacing = 16;   // words between entries: one 128-byte L2 line per entry (the
+                                     // atomics of different entries do not serialise on a line)
+constexpr int kColAccStride = kColAccMax * kColAccSpacing;
+constexpr size_t kSweepSyncBytes = 128 + 3 * size_t(kColAccStride) * sizeof(unsigned long long);
 
 template <typename T>
 struct SweepArgs {
@@ -150,7 +158,7 @@ struct SweepArgs {
   double* trace_pgrad;     // [max_iter + 1]
   unsigned long long* trace_time;  // [max_iter + 1]
   long long* status;       // [0] = last completed sweep, [1] = stopped flag
-  unsigned* barrier;       // zeroed before launch
+  unsigned* barrier;       // sync block (kSweepSyncBytes), zeroed before launch
   double* part;            // [2 * sweep_part_len(l,k) * grid]  (two alternating slots)
   double* fin;             // [2 * sweep_part_len(l,k)]
   long long* prof;         // optional: per-phase cycle counters of CTA 0 (kSweepProfSlots)

@@ -63,9 +63,9 @@ template <typename T>
 SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
   SmemLayout L{};
   size_t d = 0;
-  auto take = [&](size_t count) {
+  auto take = [&](size_t count) {  // 16-byte aligned (double2 loads)
     const size_t off = d;
-    d += count;
+    d += (count + 1) / 2 * 2;
     return off;
   };
   L.wt = take(size_t(l) * (k + 1));
@@ -120,6 +120,8 @@ struct Sweeper {
   T *WsT, *Bc, *Hc, *Rc;
   unsigned epoch = 0;
   int slot = 0;
+  unsigned long long* colacc;  // fixed-point column accumulators (3-slot ring)
+  unsigned cstep = 0;          // column steps done in this launch (ring position)
   double qrow[(QS && LREG > 0) ? LREG : 1];
   // optional cycle profile of CTA 0 / thread 0 (built with RNMF_SWEEP_PROF=1 and args.prof != nullptr;
   // compiled out otherwise, the runtime test alone costs a reconvergence point per tick)
@@ -172,6 +174,7 @@ struct Sweeper {
     Bc = reinterpret_cast<T*>(smem + L.bc);
     Hc = reinterpret_cast<T*>(smem + L.hc);
     Rc = reinterpret_cast<T*>(smem + L.rc);
+    colacc = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(a.barrier) + 128);
     part_slot_len = sweep_part_len(l, k) * G;
     fin_slot_len = sweep_part_len(l, k);
     prof_on = kSweepProf && a.prof != nullptr && g == 0 && tid == 0;
@@ -278,6 +281,62 @@ struct Sweeper {
     reduce_all(L, wr);
     next_slot();
     __syncthreads();
+    prof_tick(kPfReduce1);
+  }
+
+  // Column-step all-reduce of [Q^T W(:,j); ||W(:,j)||^2] (L1 = l + 1 entries; thread e < L1 holds
+  // the CTA's partial v of entry e).  Each partial becomes a 64-bit fixed-point integer and is
+  // added with one integer atomic into its entry's accumulator (one 128-byte L2 line per entry, so
+  // the G atomics of different entries proceed in parallel); after ONE grid barrier every CTA
+  // reads the L1 sums.  Integer addition is exact and associative, so the sums have the same bits
+  // whatever the arrival order: deterministic, bitwise-identical W~ on every CTA, without reading
+  // G partial vectors (the ordered-partials path, kColOrdered, is kept as a testing knob).
+  //   Scale: Q has orthonormal columns, so ||W(:,j)|| <= ||Q colnew|| = ||colnew|| =: B, and every
+  //   partial -- and every sum of partials over any subset of CTAs -- of entry i < l is bounded by
+  //   B, of the norm entry by B^2 (Cauchy-Schwarz over the rows involved).  With the margin 2B
+  //   and scale 2^(54 - e), 2B < 2^e, all running sums stay below 2^54 in magnitude; the quantum
+  //   2^(e-54) ~ 2^-53 * 2B is at the fp64 rounding level of an ordered sum of the partials.
+  //   Ring: 3 slots; CTA 0 zeroes the next step's slot before it arrives here -- every CTA read
+  //   that slot two steps ago, before arriving at the previous step's barrier.
+  // wr(e, value) runs on thread e; the caller synchronises the block afterwards.
+  // col_scales: the fixed-point scales from the per-warp ||colnew||^2 by exponent arithmetic (no
+  // sqrt / frexp): with b2 in [2^(E-1023), 2^(E-1022)), 2 sqrt(b2) < 2^e1 and 4 b2 < 2^e2; entries
+  // < l are scaled by 2^(54-e1), the norm entry by 2^(54-e2), clamped to the normal range (a norm
+  // below 2^-1000 then quantises to 0).  Call after the block barrier that follows col_prepare.
+  __device__ __forceinline__ void col_scales(double (&sc)[2], double (&inv)[2]) const {
+    double b2 = 0.0;
+    for (int w = 0; w * 32 < l; ++w) b2 += scal[4 + w];
+    const int E = int((__double_as_longlong(b2) >> 52) & 0x7ff);
+    const int e1 = 1 + ((E - 1021) >> 1);  // 1 + ceil((E - 1022) / 2), arithmetic shift
+    const int e2 = E - 1020;
+    const int s1 = min(1000, max(-1000, 54 - e1)), s2 = min(1000, max(-1000, 54 - e2));
+    sc[0] = __longlong_as_double(static_cast<long long>(s1 + 1023) << 52);
+    sc[1] = __longlong_as_double(static_cast<long long>(s2 + 1023) << 52);
+    inv[0] = __longlong_as_double(static_cast<long long>(1023 - s1) << 52);
+    inv[1] = __longlong_as_double(static_cast<long long>(1023 - s2) << 52);
+  }
+
+  template <typename Writer>
+  __device__ void col_allreduce(int L1, double v, const double (&sc)[2], const double (&inv)[2], Writer&& wr) {
+    if (a.flags & kColOrdered) {
+      if (tid < L1) part_base()[int64_t(g) * L1 + tid] = v;
+      allreduce1(L1, wr);
+      return;
+    }
+    unsigned long long* cur = colacc + (cstep % 3) * kColAccStride + tid * kColAccSpacing;
+    if (tid < L1) {
+      const long long fx = __double2ll_rn(v * sc[tid < l ? 0 : 1]);  // exact power-of-two scaling
+      atomicAdd(cur, static_cast<unsigned long long>(fx));
+    }
+    if (g == 0 && tid < L1) colacc[((cstep + 1) % 3) * kColAccStride + tid * kColAccSpacing] = 0ull;
+    prof_tick(kPfOther);
+    barrier();
+    prof_tick(kPfBarrier1);
+    if (tid < L1) {
+      const long long sum = static_cast<long long>(ld_cg(cur));
+      wr(tid, double(sum) * inv[tid < l ? 0 : 1]);
+    }
+    ++cstep;
     prof_tick(kPfReduce1);
   }
 
@@ -486,18 +545,33 @@ struct Sweeper {
     __syncthreads();
   }
 
-  // One column step of rhals_w_component (p/src/rhals.cpp:23-32).
+  // Column-j prologue of rhals_w_component (p/src/rhals.cpp:25-29), row-local to thread i < l:
+  // colnew(i) = W~(i,j) + (T(i,j) - P(i,j) - alpha W~(i,j)) / denom_j, plus the per-warp
+  // ||colnew||^2 that bounds the fixed-point column reduction (fixed order: identical on every
+  // CTA).  Caller synchronises before colnew is read by other threads.
+  __device__ void col_prepare(int j) {
+    const double alpha = a.alpha_w;
+    const double denom = fmax(Vm[j * k + j] + alpha, kDivisionFloor);
+    if (wid * 32 < l) {
+      double nw = 0.0;
+      if (tid < l) {
+        const double cur = Wt[tid * kp + j];
+        nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) / denom;
+        colold[tid] = cur;
+        colnew[tid] = nw;
+      }
+      const double sq = warp_allreduce_sum(nw * nw);
+      if (lane == 0) scal[4 + wid] = sq;
+    }
+  }
+
+  // One column step of rhals_w_component (p/src/rhals.cpp:23-32); col_prepare(j) has run.
   __device__ void w_column(int j) {
     const double alpha = a.alpha_w, beta = a.beta_w;
     const double denom = fmax(Vm[j * k + j] + alpha, kDivisionFloor);
-    if (tid < l) {
-      const double cur = Wt[tid * kp + j];
-      const double nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) / denom;
-      colold[tid] = cur;
-      colnew[tid] = nw;
-    }
-    __syncthreads();
     prof_tick(kPfWStep);
+    double sc[2], inv[2];
+    col_scales(sc, inv);
     const double shift = beta != 0.0 ? beta / denom : 0.0;
     const int L1 = l + 1;
     if constexpr (QS && LREG > 0) {
@@ -681,24 +755,32 @@ struct Sweeper {
     }
     }
     __syncthreads();
-    if (tid < L1) {
-      double v = 0.0;
-      for (int w = 0; w < kSwWarps; ++w) v += red[w * kRedStride + tid];
-      part_base()[int64_t(g) * L1 + tid] = v;
-    }
+    double cpart = 0.0;
+    if (tid < L1)
+      for (int w = 0; w < kSwWarps; ++w) cpart += red[w * kRedStride + tid];
     prof_tick(kPfRecomp);
-    allreduce1(L1, [&](int e, double v) {
-      if (e < l)
-        colnew[e] = v;
-      else
+    // W~(:,j) <- Q^T W(:,j) and P(i,:) += (W~_new(i,j) - W~_old(i,j)) V(j,:): thread i owns row i
+    // of W~ and P, so the next column's prologue follows without a block barrier
+    col_allreduce(L1, cpart, sc, inv, [&](int e, double v) {
+      if (e < l) {
+        const double d = v - colold[e];
+        Wt[e * kp + j] = v;
+        double* pe = Pm + e * kp;
+        const double* vj = Vm + j * k;
+        int c = 0;
+        for (; c + 8 <= k; c += 8) {
+          double pv[8], vv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pv[u] = pe[c + u], vv[u] = vj[c + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pe[c + u] = pv[u] + d * vv[u];
+        }
+        for (; c < k; ++c) pe[c] += d * vj[c];
+      } else {
         wn[j] = v;
+      }
     });
-    // W~(:,j) <- Q^T W(:,j); P += (W~_new(:,j) - W~_old(:,j)) V(j,:)
-    for (int e = tid; e < l * k; e += kSwThreads) {
-      const int i = e / k, c = e % k;
-      Pm[i * kp + c] += (colnew[i] - colold[i]) * Vm[j * k + c];
-    }
-    if (tid < l) Wt[tid * kp + j] = colnew[tid];
+    if (j + 1 < k) col_prepare(j + 1);
     __syncthreads();
   }
 
@@ -1017,6 +1099,8 @@ struct Sweeper {
       for (int64_t t = a.t_begin; t <= a.t_end; ++t) {
         if (a.flags & kDoW) {
           compute_p();
+          col_prepare(0);
+          __syncthreads();
           for (int j = 0; j < k; ++j) w_column(j);
         }
         if (a.flags & kDoH) {
@@ -1084,8 +1168,11 @@ template <typename T>
 int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream) {
   if (plan.grid <= 0) throw CudaError("sweeps: problem does not fit the persistent kernel");
   const SmemLayout L = make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem);
-  RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, sizeof(unsigned), stream));
+  RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, kSweepSyncBytes, stream));
+  if (args.l + 1 > kColAccMax) throw CudaError("sweeps: sketch width above the column-reduction capacity");
   SweepArgs<T> a = args;
+  // RNMF_COL_ORDERED: testing knob, column-step reduction through the ordered partial buffers
+  if (std::getenv("RNMF_COL_ORDERED")) a.flags |= kColOrdered;
   int64_t RM = plan.rows_per_cta, NCM = plan.cols_per_cta;
   void* kargs[] = {&a, const_cast<SmemLayout*>(&L), &RM, &NCM};
   const void* stream64 = nullptr;

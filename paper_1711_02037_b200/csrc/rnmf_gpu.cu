@@ -566,7 +566,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   a.trace_pgrad = ctx->d<double>("sw.tpgrad", size_t(max_iter + 1));
   a.trace_time = ctx->d<unsigned long long>("sw.ttime", size_t(max_iter + 1));
   a.status = ctx->d<long long>("sw.status", 2);
-  a.barrier = ctx->d<unsigned>("sw.barrier", 1);
+  a.barrier = reinterpret_cast<unsigned*>(ctx->d<unsigned long long>("sw.sync", kSweepSyncBytes / 8));
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
   // RNMF_PROF=1: per-phase cycle counters of CTA 0, printed to stderr (development aid)
@@ -798,7 +798,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
     a.trace_pgrad = ctx->d<double>("sw.tpgrad", 1);
     a.trace_time = ctx->d<unsigned long long>("sw.ttime", 1);
     a.status = ctx->d<long long>("sw.status", 2);
-    a.barrier = ctx->d<unsigned>("sw.barrier", 1);
+    a.barrier = reinterpret_cast<unsigned*>(ctx->d<unsigned long long>("sw.sync", kSweepSyncBytes / 8));
     const int64_t plen = sweep_part_len(l, k);
     a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
     a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
@@ -913,7 +913,7 @@ static void stage_impl(rnmf_gpu_context* ctx, int location, const rnmf_problem_s
   a.trace_pgrad = ctx->d<double>("sw.tpgrad", 2);
   a.trace_time = ctx->d<unsigned long long>("sw.ttime", 2);
   a.status = ctx->d<long long>("sw.status", 2);
-  a.barrier = ctx->d<unsigned>("sw.barrier", 1);
+  a.barrier = reinterpret_cast<unsigned*>(ctx->d<unsigned long long>("sw.sync", kSweepSyncBytes / 8));
   const int64_t plen = sweep_part_len(l, k);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
