@@ -2,6 +2,7 @@
 // Every wrapper enqueues on `stream` and returns the number of kernels it launched.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -56,12 +57,18 @@ int launch_grad_h_reduce(const T* part, int splits, int64_t n, int k, const T* h
 
 // ---- fused one-pass metrics (kernels_metrics.cu): objective from the explicit residual, projected
 // grad_W, and (when wtx_part != nullptr) per-CTA partials of W^T X (metrics_grid(m) x n x k).
-int metrics_tiles(int64_t m);
-int metrics_grid(int64_t m, int sm_count);
+// X (pitch ldx, 16-byte aligned rows) and a zero-padded copy of H (metrics_hpad_len(k, n) elements of
+// scratch `hpad`) are streamed by TMA.
+int metrics_grid(int64_t m, int k, int elem_bytes, int sm_count);
+int64_t metrics_hpad_len(int k, int64_t n);
 template <typename T>
 int launch_metrics_fused(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w, const T* h, int k,
-                         const double* hht, T* wtx_part, double* part_obj, double* part_pgw, int sm_count,
+                         const double* hht, T* hpad, T* wtx_part, double* part_obj, double* part_pgw, int sm_count,
                          cudaStream_t stream);
+// 2-D row-major tensor map (rows x cols, pitch in elements), box = box_rows x box_cols, no swizzle,
+// zero fill out of bounds (kernels_tc.cu)
+CUtensorMap make_tma_2d(const void* base, int elem_bytes, int64_t rows, int64_t cols, int64_t pitch, int box_cols,
+                        int box_rows);
 
 // ---- small dense helpers (kernels_xgemm.cu) ---------------------------------------------------
 // G (c x c, fp64) = A^T A for A (rows x c) row-major.  part: gram_parts(rows)*c*c doubles.

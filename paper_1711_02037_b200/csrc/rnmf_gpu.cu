@@ -458,7 +458,8 @@ class Engine {
     // one fused X pass when the per-tile W^T X partials stay small (<= 1/4 of X), else the fused
     // pass without W^T X plus a split-K X^T W pass
     const bool fused_ok = k <= 64 && (sizeof(T) == 4 || k <= 32);
-    const double wtx_bytes = double(metrics_grid(m, ctx_->sm_count)) * double(n) * k * sizeof(T);
+    const int g1 = metrics_grid(m, k, int(sizeof(T)), ctx_->sm_count);
+    const double wtx_bytes = double(g1) * double(n) * k * sizeof(T);
     const bool one_pass = fused_ok && wtx_bytes <= 0.25 * double(m) * double(n) * sizeof(T);
     x_passes_ = 2;
     tm_.span(kMetrics, [&] {
@@ -466,17 +467,17 @@ class Engine {
       tm_.launches += launch_gram_rows<T>(w, m, k, gpart2, wtw, st_);
       int b1 = 0, b2 = 0;
       if (fused_ok) {
-        T* wtx = one_pass ? ctx_->d<T>("met.wtx", size_t(metrics_grid(m, ctx_->sm_count)) * n * k) : nullptr;
-        const int g1 = metrics_grid(m, ctx_->sm_count);
+        T* wtx = one_pass ? ctx_->d<T>("met.wtx", size_t(g1) * n * k) : nullptr;
+        T* hpad = ctx_->d<T>("met.hpad", size_t(metrics_hpad_len(k, n)));
         double* po = ctx_->d<double>("met.pobj2", size_t(g1));
         double* pw = ctx_->d<double>("met.ppgw2", size_t(g1));
-        tm_.launches += launch_metrics_fused<T>(x, m, n, ldx, w, h, k, hht, wtx, po, pw, ctx_->sm_count, st_);
+        tm_.launches += launch_metrics_fused<T>(x, m, n, ldx, w, h, k, hht, hpad, wtx, po, pw, ctx_->sm_count, st_);
         b1 = g1;
         pobj = po;
         ppgw = pw;
         if (one_pass) {
           double* pgh = ctx_->d<double>("met.ppgh2", size_t(ceil_div(n * k, 256)));
-          tm_.launches += launch_grad_h_reduce<T>(wtx, metrics_grid(m, ctx_->sm_count), n, k, h, wtw, pgh, &b2, st_);
+          tm_.launches += launch_grad_h_reduce<T>(wtx, g1, n, k, h, wtw, pgh, &b2, st_);
           ppgh = pgh;
           x_passes_ = 1;
         } else {
