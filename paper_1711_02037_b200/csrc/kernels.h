@@ -50,7 +50,9 @@ int launch_xtw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w
                        const double* wtw, T* part, int splits, double* part_pgh, int* nblocks,
                        cudaStream_t stream);
 
-// grad_H projected norm from W^T X split partials part[s][n][k] (fixed-order sum over s)
+// grad_H projected norm from W^T X split partials part[s][n][k] (fixed-order sum over s);
+// writes grad_h_blocks(n, k) partial sums to part_pgh
+int64_t grad_h_blocks(int64_t n, int k);
 template <typename T>
 int launch_grad_h_reduce(const T* part, int splits, int64_t n, int k, const T* h, const double* wtw, double* part_pgh,
                          int* nblocks, cudaStream_t stream);

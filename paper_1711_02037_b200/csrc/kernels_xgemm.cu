@@ -416,41 +416,56 @@ __global__ void splitk_reduce_kernel(const T* __restrict__ part, int splits, int
 // Metrics grad_H epilogue: for each (X column col, j), sum the split partials of (W^T X)(j, col) in
 // fixed order, form grad_H(j, col) = -2 ((W^T X)(j, col) - ((W^T W) H)(j, col)), project by
 // H(j, col), square; one partial sum per CTA.
+// grad_H = -2 (sum_s part[s] - (W^T W) H), projected: a block covers 64 (col, j) entries with 4
+// split groups each (group g sums s = g, g + 4, ... with 4 independent accumulators, all loads of
+// an unrolled step in flight); the groups are combined in fixed order (deterministic).
+constexpr int kGhEntries = 64, kGhGroups = kThreads / kGhEntries;
 template <typename T>
 __global__ void __launch_bounds__(kThreads) xtw_metrics_reduce_kernel(const T* __restrict__ part, int splits,
                                                                       int64_t n, int k,
                                                                       const T* __restrict__ H,
                                                                       const double* __restrict__ wtw,
                                                                       double* part_pgh) {
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // e = col * k + j
+  __shared__ double gsum[kGhGroups][kGhEntries];
+  __shared__ double red[kThreads / 32];
+  const int ei = threadIdx.x % kGhEntries, gi = threadIdx.x / kGhEntries;
+  const int64_t e = int64_t(blockIdx.x) * kGhEntries + ei;  // e = col * k + j
+  const int64_t total = n * k;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  if (e < total) {
+    int s = gi;
+    for (; s + 3 * kGhGroups < splits; s += 4 * kGhGroups) {
+      T v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = part[int64_t(s + u * kGhGroups) * total + e];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] += double(v[u]);
+    }
+    for (; s < splits; s += kGhGroups) a[0] += double(part[int64_t(s) * total + e]);
+  }
+  gsum[gi][ei] = (a[0] + a[1]) + (a[2] + a[3]);
+  __syncthreads();
   double acc = 0.0;
-  if (e < n * k) {
+  if (gi == 0 && e < total) {
+    double wx = 0.0;
+#pragma unroll
+    for (int g = 0; g < kGhGroups; ++g) wx += gsum[g][ei];
     const int64_t col = e / k;
     const int j = int(e % k);
-    const int64_t total = n * k;
-    double a0 = 0.0, a1 = 0.0;
-    int s = 0;
-    for (; s + 1 < splits; s += 2) {
-      a0 += double(part[int64_t(s) * total + e]);
-      a1 += double(part[int64_t(s + 1) * total + e]);
-    }
-    if (s < splits) a0 += double(part[int64_t(s) * total + e]);
-    const double a = a0 + a1;
     double b = 0.0;
     for (int t = 0; t < k; ++t) b += wtw[j * k + t] * double(H[int64_t(t) * n + col]);
-    const double g = -2.0 * (a - b);
+    const double g = -2.0 * (wx - b);
     const double hv = double(H[int64_t(j) * n + col]);
     const double gp = hv > 0.0 ? g : fmin(g, 0.0);
     acc = gp * gp;
   }
-  __shared__ double red[kThreads / 32];
   acc = warp_allreduce_sum(acc);
   if (lane_id() == 0) red[warp_id()] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) a += red[w];
-    part_pgh[blockIdx.x] = a;
+    double t = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+    part_pgh[blockIdx.x] = t;
   }
 }
 
@@ -697,7 +712,7 @@ int launch_xtw_metrics(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w
 template <typename T>
 int launch_grad_h_reduce(const T* part, int splits, int64_t n, int k, const T* h, const double* wtw, double* part_pgh,
                          int* nblocks, cudaStream_t stream) {
-  const int blocks = int(ceil_div(n * k, kThreads));
+  const int blocks = int(ceil_div(n * k, kGhEntries));
   xtw_metrics_reduce_kernel<T><<<blocks, kThreads, 0, stream>>>(part, splits, n, k, h, wtw, part_pgh);
   RNMF_CUDA_LAUNCH();
   *nblocks = blocks;
@@ -713,7 +728,9 @@ int launch_splitk_reduce(const T* part, int splits, int64_t n, int c, T* out, bo
   return 1;
 }
 
-int gram_parts(int64_t len) { return int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(len, 256)))); }
+int64_t grad_h_blocks(int64_t n, int k) { return ceil_div(n * k, kGhEntries); }
+
+int gram_parts(int64_t len) { return int(std::max<int64_t>(1, std::min<int64_t>(296, ceil_div(len, 16)))); }
 
 template <typename T>
 int launch_gram_rows(const T* a, int64_t rows, int c, double* part, double* g, cudaStream_t stream) {

@@ -453,7 +453,7 @@ class Engine {
     double* ppgw = ctx_->d<double>("met.ppgw", size_t(nb1));
     const int splits = xtw_default_splits(m, n);
     T* part = ctx_->d<T>("met.part", size_t(splits) * n * k);
-    double* ppgh = ctx_->d<double>("met.ppgh", size_t(ceil_div(n * k, 256)));
+    double* ppgh = ctx_->d<double>("met.ppgh", size_t(grad_h_blocks(n, k)));
     double* tmp = ctx_->d<double>("met.tmp", 4);
     // one fused X pass when the per-tile W^T X partials stay small (<= 1/4 of X), else the fused
     // pass without W^T X plus a split-K X^T W pass
@@ -476,12 +476,12 @@ class Engine {
         pobj = po;
         ppgw = pw;
         if (one_pass) {
-          double* pgh = ctx_->d<double>("met.ppgh2", size_t(ceil_div(n * k, 256)));
+          double* pgh = ctx_->d<double>("met.ppgh2", size_t(grad_h_blocks(n, k)));
           tm_.launches += launch_grad_h_reduce<T>(wtx, g1, n, k, h, wtw, pgh, &b2, st_);
           ppgh = pgh;
           x_passes_ = 1;
         } else {
-          double* pgh = ctx_->d<double>("met.ppgh2", size_t(ceil_div(n * k, 256)));
+          double* pgh = ctx_->d<double>("met.ppgh2", size_t(grad_h_blocks(n, k)));
           tm_.launches += launch_xtw_metrics<T>(x, m, n, ldx, w, k, h, wtw, part, splits, pgh, &b2, st_);
           ppgh = pgh;
         }
