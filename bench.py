@@ -93,6 +93,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
+def load_traffic(cfg_name: str):
+    """DRAM bytes per launch of the X-streaming kernels from the committed ncu --set full summary
+    (profiles/latest_traffic.json, written by tools/ncu_summary.py); None if absent."""
+    p = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(cfg_name)
+    except Exception:
+        return None
+
+
 def make_workload(cfg_name: str, device):
     """X (device, fp32/fp64), injected Omega / unscaled init draws, solver options."""
     import torch
@@ -293,6 +305,8 @@ def main():
     sk_bytes = agg["xw_bytes"] + agg["xtw_bytes"]
     sk_ms = agg["xw_ms"] + agg["xtw_ms"]
     sk_gbs = sk_bytes / (sk_ms / 1e3) / 1e9 if sk_ms > 0 else 0.0
+    met_gbs = agg["metrics_bytes"] / (agg["metrics_ms"] / 1e3) / 1e9 if agg["metrics_ms"] > 0 else 0.0
+    traffic = load_traffic(args.config)
     shares = {name: agg[name] / agg["total_ms"] for name in
               ("scan_ms", "sketch_ms", "qr_ms", "init_ms", "sweeps_ms", "metrics_ms", "h2d_ms", "d2h_ms")}
     line = {
@@ -318,10 +332,15 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "X-streaming sketch GEMMs (xw_kernel Y=X*S, xtw_kernel X^T*Q)",
                      "achieved": sk_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": sk_gbs / hbm_peak,
-                     "peak_kind": peak_kind, "traffic": None,
+                     "peak_kind": peak_kind,
+                     "traffic": traffic.get("sketch_bytes_per_launch") if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
                      "per_kernel": {"xw_gbs": xw_gbs, "xtw_gbs": xtw_gbs,
                                     "xw_bytes_per_launch": agg["xw_bytes"] / max(agg["xw_launches"], 1),
-                                    "xtw_bytes_per_launch": agg["xtw_bytes"] / max(agg["xtw_launches"], 1)}},
+                                    "xtw_bytes_per_launch": agg["xtw_bytes"] / max(agg["xtw_launches"], 1),
+                                    "metrics_pass_gbs": met_gbs,
+                                    "metrics_bytes_per_eval": agg["metrics_bytes"] / max(agg["metrics_passes"], 1),
+                                    "ncu_dram_bytes_per_launch": traffic.get("kernels") if traffic else None}},
         "stage_ms": {key: agg[key] for key in ("scan_ms", "sketch_ms", "qr_ms", "init_ms", "sweeps_ms", "metrics_ms",
                                                "xw_ms", "xtw_ms", "h2d_ms", "d2h_ms", "total_ms")},
         "stage_share": shares,

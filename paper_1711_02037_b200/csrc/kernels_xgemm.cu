@@ -540,12 +540,28 @@ __global__ void __launch_bounds__(kThreads) gram_cols_kernel(const T* __restrict
   }
 }
 
-__global__ void reduce_parts_kernel(const double* __restrict__ part, int nparts, int len, double* out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= len) return;
-  double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += part[int64_t(p) * len + e];
-  out[e] = s;
+// out[e] = sum_p part[p][e]: a block covers 64 entries x 4 part groups (4 independent loads in
+// flight per thread), groups combined in fixed order (deterministic)
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nparts, int len,
+                                                           double* out) {
+  __shared__ double gs[4][64];
+  const int ei = threadIdx.x % 64, gi = threadIdx.x / 64;
+  const int e = blockIdx.x * 64 + ei;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  if (e < len) {
+    int p = gi;
+    for (; p + 12 < nparts; p += 16) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = part[int64_t(p + 4 * u) * len + e];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] += v[u];
+    }
+    for (; p < nparts; p += 4) a[0] += part[int64_t(p) * len + e];
+  }
+  gs[gi][ei] = (a[0] + a[1]) + (a[2] + a[3]);
+  __syncthreads();
+  if (gi == 0 && e < len) out[e] = ((gs[0][ei] + gs[1][ei]) + gs[2][ei]) + gs[3][ei];
 }
 
 template <typename T>
@@ -739,7 +755,7 @@ int launch_gram_rows(const T* a, int64_t rows, int c, double* part, double* g, c
   const size_t sm = size_t(kGramChunk) * c * sizeof(double);
   gram_rows_kernel<T><<<np, kThreads, sm, stream>>>(a, rows, c, part);
   RNMF_CUDA_LAUNCH();
-  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 256)), 256, 0, stream>>>(part, np, c * c, g);
+  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 64)), 256, 0, stream>>>(part, np, c * c, g);
   RNMF_CUDA_LAUNCH();
   return 2;
 }
@@ -751,7 +767,7 @@ int launch_gram_cols(const T* a, int c, int64_t cols, double* part, double* g, c
   const size_t sm = size_t(kGramChunk) * c * sizeof(double);
   gram_cols_kernel<T><<<np, kThreads, sm, stream>>>(a, c, cols, part);
   RNMF_CUDA_LAUNCH();
-  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 256)), 256, 0, stream>>>(part, np, c * c, g);
+  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 64)), 256, 0, stream>>>(part, np, c * c, g);
   RNMF_CUDA_LAUNCH();
   return 2;
 }
