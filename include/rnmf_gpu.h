@@ -221,6 +221,32 @@ int rnmf_gpu_rhals_update_H(rnmf_gpu_context* ctx, int dtype, int location,
                             const void* wt, const void* w, void* h, const rnmf_reg_config* reg,
                             char* err, size_t err_cap);
 
+/* ---- multi-GPU: X sharded by rows, one process per GPU ------------------------ *
+ * The reference is single-process/single-node; these entries extend rhals_fit to X row-sharded
+ * over `world` GPUs of one node.  Rank 0 calls rnmf_gpu_comm_unique_id and the host program
+ * hands the 128 bytes to every rank (e.g. torch.distributed.broadcast_object_list); each rank
+ * then creates its context (collective: NCCL communicator + CUDA IPC mapping of the peers' sweep
+ * sync blocks) and calls rnmf_gpu_rhals_fit_sharded with the same options (collective).
+ * Exchanges: Gram all-reduces inside CholeskyQR (shifted CholeskyQR3 replaces the TSQR fallback),
+ * NCCL all-reduces of X^T Q, Q^T X, W^T W, W^T X and the metrics scalars; inside the persistent
+ * sweep kernel every column step adds its fixed-point partials into every GPU's accumulators with
+ * integer atomics over NVLink (order-free: all GPUs hold bitwise-identical W~), and the
+ * W~-init / grad_W sums go through a rank-ordered exchange buffer.  H, B, T, V, E are replicated. */
+#define RNMF_COMM_ID_BYTES 128
+int rnmf_gpu_comm_unique_id(unsigned char* id_out, char* err, size_t err_cap);
+int rnmf_gpu_context_create_sharded(int device, int rank, int world, const unsigned char* id,
+                                    rnmf_gpu_context** out, char* err, size_t err_cap);
+/* Rows [row_offset, row_offset + m_local) of an m_total x n matrix on this rank.  w0_local: this
+ * rank's rows of the unscaled W draw (NULL: the reference stream, of which this rank keeps its
+ * rows); omega, h0 as in rnmf_gpu_rhals_fit (identical on every rank).  w_out: m_local x k rows,
+ * h_out: k x n (replicated), trace identical on every rank. */
+int rnmf_gpu_rhals_fit_sharded(rnmf_gpu_context* ctx, const void* x_local, int dtype, int location,
+                               int64_t m_local, int64_t row_offset, int64_t m_total, int64_t n,
+                               const rnmf_solver_options* opts, const double* omega,
+                               const double* w0_local, const double* h0, void* w_out, void* h_out,
+                               rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len,
+                               char* err, size_t err_cap);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+
 namespace rnmf_gpu {
 
 // ---- validation / mean / norm pass over X (kernels_scan.cu) ---------------------------------
@@ -91,6 +93,8 @@ template <typename T>
 int launch_widen(const T* in, int64_t count, double* out, cudaStream_t stream);
 // sum of `count` doubles in fixed order -> out[0]
 int launch_sum_parts(const double* part, int count, double* out, cudaStream_t stream);
+// out[e] = sum_p part[p * len + e], fixed order
+int launch_reduce_parts(const double* part, int nparts, int len, double* out, cudaStream_t stream);
 // writes %globaltimer to *out
 int launch_timestamp(unsigned long long* out, cudaStream_t stream);
 
@@ -122,8 +126,13 @@ int tsqr_max_l(int max_smem);
 // Q (rows x l) of A via two fp64-Gram CholeskyQR passes; *flag (device) is set non-zero when A is
 // too ill-conditioned for CholeskyQR2 (the caller then runs TSQR).  l <= 128.
 int64_t cholqr_workspace_doubles(int64_t rows, int l);
+// Row-sharded QR: `allreduce` sums the l x l fp64 Gram (device) over the GPUs holding the other
+// rows before every Cholesky.  shift_rel > 0: shifted CholeskyQR3 (G + shift_rel * trace(G) * I in
+// the first pass, then two plain passes) -- the sharded replacement of the TSQR fallback.
+using GramAllreduce = std::function<void(double* gram, int64_t count)>;
 template <typename T>
-int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream);
+int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream,
+                   const GramAllreduce* allreduce = nullptr, double shift_rel = 0.0);
 
 // ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cu) -----------------------------
 enum SweepFlags : int {
@@ -142,7 +151,14 @@ constexpr int kColAccMax = 136;      // entries per slot, >= l + 1
 constexpr int kColAccSpacing = 16;   // words between entries: one 128-byte L2 line per entry (the
                                      // atomics of different entries do not serialise on a line)
 constexpr int kColAccStride = kColAccMax * kColAccSpacing;
+// zeroed part: local barrier counter (byte 0), cross-GPU barrier counter (byte 64), accumulators
 constexpr size_t kSweepSyncBytes = 128 + 3 * size_t(kColAccStride) * sizeof(unsigned long long);
+// Row-sharded runs (one process per GPU): after the zeroed part, a 2-slot exchange buffer of
+// kMaxWorld x kXMax doubles per slot that peers write into (never needs clearing).
+constexpr int kMaxWorld = 8;
+constexpr int kXMax = 128 * 64 + 64;  // >= l * k + k
+constexpr size_t kSweepXbufOffset = kSweepSyncBytes;
+constexpr size_t kSweepSyncTotal = kSweepSyncBytes + 2 * size_t(kMaxWorld) * kXMax * sizeof(double);
 
 template <typename T>
 struct SweepArgs {
@@ -167,7 +183,13 @@ struct SweepArgs {
   double* trace_pgrad;     // [max_iter + 1]
   unsigned long long* trace_time;  // [max_iter + 1]
   long long* status;       // [0] = last completed sweep, [1] = stopped flag
-  unsigned* barrier;       // sync block (kSweepSyncBytes), zeroed before launch
+  unsigned* barrier;       // sync block (kSweepSyncTotal; the first kSweepSyncBytes zeroed before launch)
+  // row sharding: this process is `rank` of `world` GPUs; peer_sync[p] = GPU p's sync block mapped
+  // into this process (peer_sync[rank] = barrier); xtotal = sum of the grids of all ranks.
+  // world == 0: single-GPU kernel (no cross-GPU steps).
+  int world, rank;
+  long long xtotal;
+  unsigned char* peer_sync[kMaxWorld];
   double* part;            // [2 * sweep_part_len(l,k) * grid]  (two alternating slots)
   double* fin;             // [2 * sweep_part_len(l,k)]
   long long* prof;         // optional: per-phase cycle counters of CTA 0 (kSweepProfSlots)

@@ -12,6 +12,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace rnmf_gpu {
 
@@ -69,7 +70,8 @@ __global__ void __launch_bounds__(kCqThreads) cq_gram_kernel(const T* __restrict
 // flag |= 1 when a pivot collapses; with `check_identity`, flag |= 2 when max|R - I| > 1e-2 (the
 // second CholeskyQR pass must see an almost orthonormal input).
 __global__ void __launch_bounds__(kCqThreads) cq_chol_kernel(const double* __restrict__ part, int nparts, int l,
-                                                             double* __restrict__ rinv, int* flag, int check_identity) {
+                                                             double* __restrict__ rinv, int* flag, int check_identity,
+                                                             double shift_rel) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lp = l + 1;
   double* G = reinterpret_cast<double*>(smem);  // [l][lp], becomes R in its upper triangle
@@ -81,7 +83,14 @@ __global__ void __launch_bounds__(kCqThreads) cq_chol_kernel(const double* __res
     for (int p = 0; p < nparts; ++p) s += part[int64_t(p) * ll + e];
     G[(e / l) * lp + e % l] = s;
   }
-  if (threadIdx.x == 0) bad = 0;
+  if (threadIdx.x == 0) {
+    bad = 0;
+    if (shift_rel > 0.0) {  // shifted Cholesky: G + s I, s = shift_rel * trace(G) >= shift_rel * ||G||_2
+      double tr = 0.0;
+      for (int j = 0; j < l; ++j) tr += G[j * lp + j];
+      for (int j = 0; j < l; ++j) G[j * lp + j] += shift_rel * tr;
+    }
+  }
   __syncthreads();
   // right-looking Cholesky on the upper triangle: row j of R, then the trailing update
   for (int j = 0; j < l; ++j) {
@@ -110,7 +119,7 @@ __global__ void __launch_bounds__(kCqThreads) cq_chol_kernel(const double* __res
       mx = fmax(mx, fabs(G[j * lp + j]));
       mn = fmin(mn, fabs(G[j * lp + j]));
     }
-    if (!(mn > 1e-6 * mx)) bad = 1;  // R diag ratio ~ 1/cond(A); CholeskyQR2 needs cond << 1e8
+    if (!(mn > 1e-6 * mx) && shift_rel == 0.0) bad = 1;  // R diag ratio ~ 1/cond(A); needs cond << 1e8
   }
   // Rinv by column-wise back substitution (thread per column)
   for (int c = threadIdx.x; c < l; c += kCqThreads) {
@@ -183,7 +192,8 @@ int64_t cholqr_workspace_doubles(int64_t rows, int l) {
 }
 
 template <typename T>
-int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream) {
+int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream,
+                   const GramAllreduce* allreduce, double shift_rel) {
   const int nb = gram_blocks(rows);
   double* part = ws;
   double* rinv1 = part + int64_t(nb) * l * l;
@@ -197,27 +207,55 @@ int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* f
   RNMF_CUDA(cudaFuncSetAttribute(cq_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
   RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
   RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
+  RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(asm_)));
   RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
   RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
   const int ab = int(std::max<int64_t>(1, std::min<int64_t>(148 * 4, ceil_div(rows, 64))));
+  int launches = 0;
+  // Gram partials -> (sharded: one local Gram, summed over the GPUs) -> Cholesky -> R^-1
+  auto chol = [&](auto* src, double* rinv, int check_identity, double shift) {
+    cq_gram_kernel<std::remove_const_t<std::remove_pointer_t<decltype(src)>>><<<nb, kCqThreads, gsm, stream>>>(
+        src, rows, l, part);
+    RNMF_CUDA_LAUNCH();
+    int np = nb;
+    if (allreduce) {
+      launches += launch_reduce_parts(part, nb, l * l, part + int64_t(nb) * 0, stream);  // in place: part[0]
+      (*allreduce)(part, int64_t(l) * l);
+      np = 1;
+    }
+    cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, np, l, rinv, flag, check_identity, shift);
+    RNMF_CUDA_LAUNCH();
+    launches += 2;
+  };
+  if (shift_rel > 0.0) {
+    // shifted CholeskyQR3: the shifted pass makes Q1 well conditioned, two plain passes follow
+    double* q0 = q1;
+    chol(a, rinv1, 0, shift_rel);
+    cq_apply_kernel<T, double><<<ab, kCqThreads, asm_, stream>>>(a, rows, l, rinv1, q0);
+    RNMF_CUDA_LAUNCH();
+    chol(static_cast<const double*>(q0), rinv2, 0, 0.0);
+    cq_apply_kernel<double, double><<<ab, kCqThreads, asm_, stream>>>(q0, rows, l, rinv2, q0);
+    RNMF_CUDA_LAUNCH();
+    chol(static_cast<const double*>(q0), rinv1, 1, 0.0);
+    cq_apply_kernel<double, T><<<ab, kCqThreads, asm_, stream>>>(q0, rows, l, rinv1, q_out);
+    RNMF_CUDA_LAUNCH();
+    return launches + 3;
+  }
   // pass 1
-  cq_gram_kernel<T><<<nb, kCqThreads, gsm, stream>>>(a, rows, l, part);
-  RNMF_CUDA_LAUNCH();
-  cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, nb, l, rinv1, flag, 0);
-  RNMF_CUDA_LAUNCH();
+  chol(a, rinv1, 0, 0.0);
   cq_apply_kernel<T, double><<<ab, kCqThreads, asm_, stream>>>(a, rows, l, rinv1, q1);
   RNMF_CUDA_LAUNCH();
   // pass 2
-  cq_gram_kernel<double><<<nb, kCqThreads, gsm, stream>>>(q1, rows, l, part);
-  RNMF_CUDA_LAUNCH();
-  cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, nb, l, rinv2, flag, 1);
-  RNMF_CUDA_LAUNCH();
+  chol(static_cast<const double*>(q1), rinv2, 1, 0.0);
   cq_apply_kernel<double, T><<<ab, kCqThreads, asm_, stream>>>(q1, rows, l, rinv2, q_out);
   RNMF_CUDA_LAUNCH();
-  return 6;
+  return launches + 2;
 }
 
-template int launch_cholqr2<float>(const float*, int64_t, int, float*, double*, int*, cudaStream_t);
-template int launch_cholqr2<double>(const double*, int64_t, int, double*, double*, int*, cudaStream_t);
+template int launch_cholqr2<float>(const float*, int64_t, int, float*, double*, int*, cudaStream_t,
+                                   const GramAllreduce*, double);
+template int launch_cholqr2<double>(const double*, int64_t, int, double*, double*, int*, cudaStream_t,
+                                    const GramAllreduce*, double);
 
 }  // namespace rnmf_gpu

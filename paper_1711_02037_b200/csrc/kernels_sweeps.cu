@@ -121,6 +121,8 @@ struct Sweeper {
   unsigned epoch = 0;
   int slot = 0;
   unsigned long long* colacc;  // fixed-point column accumulators (3-slot ring)
+  unsigned xepoch = 0;         // cross-GPU barriers passed (row-sharded runs)
+  int xslot = 0;               // exchange-buffer slot of the next cross_allreduce
   unsigned cstep = 0;          // column steps done in this launch (ring position)
   double qrow[(QS && LREG > 0) ? LREG : 1];
   // optional cycle profile of CTA 0 / thread 0 (built with RNMF_SWEEP_PROF=1 and args.prof != nullptr;
@@ -228,6 +230,49 @@ struct Sweeper {
 
   __device__ void barrier() { grid_barrier(a.barrier, epoch); }
 
+  // ---- row sharding across GPUs (a.world >= 1; one process per GPU, peers mapped by IPC) ------
+  __device__ __forceinline__ bool sharded() const { return a.world > 0; }
+  __device__ __forceinline__ unsigned* xcounter(int p) const {
+    return reinterpret_cast<unsigned*>(a.peer_sync[p] + 64);
+  }
+  __device__ __forceinline__ double* xbuf(int p, int slot_, int from) const {
+    return reinterpret_cast<double*>(a.peer_sync[p] + kSweepXbufOffset) + (int64_t(slot_) * kMaxWorld + from) * kXMax;
+  }
+  // Barrier over every CTA of every GPU: each CTA arrives (release, system scope) on the counter of
+  // every GPU and waits for its own counter to reach xepoch * (sum of all grids).
+  __device__ void xbarrier() {
+    __syncthreads();
+    xepoch += 1;
+    if (tid == 0) {
+      for (int p = 0; p < a.world; ++p) red_release_sys_add(xcounter(p), 1u);
+      const unsigned target = unsigned(xepoch * a.xtotal);
+      while (ld_acquire_sys(xcounter(a.rank)) < target) {
+      }
+    }
+    __syncthreads();
+  }
+  // All-reduce over GPUs of L values that are already identical in every CTA of a GPU (the result
+  // of a GPU-local reduction): CTA 0 stores its GPU's values into slot [xslot][rank] of every
+  // GPU's exchange buffer, one cross barrier, then every CTA sums the world contributions in rank
+  // order -- the same bits on every GPU.  put(e, v) runs after all reads of get().
+  template <typename Get, typename Put>
+  __device__ void cross_allreduce(int L, Get&& get, Put&& put) {
+    if (!sharded()) return;
+    if (g == 0)
+      for (int e = tid; e < L; e += kSwThreads) {
+        const double v = get(e);
+        for (int p = 0; p < a.world; ++p) xbuf(p, xslot, a.rank)[e] = v;
+      }
+    xbarrier();
+    for (int e = tid; e < L; e += kSwThreads) {
+      double s2 = 0.0;
+      for (int r = 0; r < a.world; ++r) s2 += __ldcg(xbuf(a.rank, xslot, r) + e);
+      put(e, s2);
+    }
+    xslot ^= 1;
+    __syncthreads();
+  }
+
   // Partial layout is CTA-major: p[g * L + e] holds CTA g's contribution to entry e of an
   // L-long vector.  wr(e, sum_g p[g][e]) for e in [e0, e1): consecutive threads take consecutive
   // entries (coalesced), S thread-slices per entry stride over g with all loads independent, and
@@ -323,14 +368,26 @@ struct Sweeper {
       allreduce1(L1, wr);
       return;
     }
-    unsigned long long* cur = colacc + (cstep % 3) * kColAccStride + tid * kColAccSpacing;
+    const int64_t off = (cstep % 3) * kColAccStride + tid * kColAccSpacing;
+    unsigned long long* cur = colacc + off;
     if (tid < L1) {
       const long long fx = __double2ll_rn(v * sc[tid < l ? 0 : 1]);  // exact power-of-two scaling
-      atomicAdd(cur, static_cast<unsigned long long>(fx));
+      if (sharded()) {
+        // the same integer atomics into every GPU's accumulator (NVLink): all GPUs end with the
+        // identical exact sum over all rows of all shards
+        for (int p = 0; p < a.world; ++p)
+          red_relaxed_sys_add_u64(reinterpret_cast<unsigned long long*>(a.peer_sync[p] + 128) + off,
+                                  static_cast<unsigned long long>(fx));
+      } else {
+        atomicAdd(cur, static_cast<unsigned long long>(fx));
+      }
     }
     if (g == 0 && tid < L1) colacc[((cstep + 1) % 3) * kColAccStride + tid * kColAccSpacing] = 0ull;
     prof_tick(kPfOther);
-    barrier();
+    if (sharded())
+      xbarrier();
+    else
+      barrier();
     prof_tick(kPfBarrier1);
     if (tid < L1) {
       const long long sum = static_cast<long long>(ld_cg(cur));
@@ -524,6 +581,16 @@ struct Sweeper {
         wn[e - lk] = v;
       }
     });
+    // row-sharded: W~ = Q^T W and ||W(:,j)||^2 are sums over the rows of every GPU
+    cross_allreduce(
+        L, [&](int e) { return e < lk ? Wt[(e / k) * kp + e % k] : wn[e - lk]; },
+        [&](int e, double v) {
+          if (e < lk) {
+            if (do_wt) Wt[(e / k) * kp + e % k] = v;
+          } else if (do_wn) {
+            wn[e - lk] = v;
+          }
+        });
   }
 
   // P = W~ V (l x k), recomputed at the start of every W phase and then kept current with a
@@ -1062,6 +1129,7 @@ struct Sweeper {
     if (tid == 0) part_base()[g] = tot;
     prof_tick(kPfPgw);
     allreduce1(1, [&](int, double v) { scal[2] = v; });
+    cross_allreduce(1, [&](int) { return scal[2]; }, [&](int, double v) { scal[2] = v; });
     const double out = scal[2];
     __syncthreads();
     return out;

@@ -796,6 +796,12 @@ int launch_widen(const T* in, int64_t count, double* out, cudaStream_t stream) {
   return 1;
 }
 
+int launch_reduce_parts(const double* part, int nparts, int len, double* out, cudaStream_t stream) {
+  reduce_parts_kernel<<<unsigned(ceil_div(len, 64)), 256, 0, stream>>>(part, nparts, len, out);
+  RNMF_CUDA_LAUNCH();
+  return 1;
+}
+
 int launch_sum_parts(const double* part, int count, double* out, cudaStream_t stream) {
   sum_parts_kernel<<<1, 32, 0, stream>>>(part, count, out);
   RNMF_CUDA_LAUNCH();

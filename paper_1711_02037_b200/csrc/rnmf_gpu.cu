@@ -6,6 +6,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is opened at run time (row-sharded contexts)
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -81,11 +84,61 @@ struct Buffer {
   size_t bytes = 0;
 };
 
+// ---- NCCL, opened at run time (only row-sharded contexts need it) --------------------------------
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // a process that already loaded NCCL (e.g. torch.distributed) shares that copy
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.error = std::string("libnccl.so.2 not loadable: ") + dlerror();
+      return a;
+    }
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.AllGather || !a.CommDestroy || !a.GetErrorString)
+      a.error = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  if (!api.error.empty()) throw CudaError("NCCL: " + api.error);
+  return api;
+}
+
+#define RNMF_NCCL(call)                                                                             \
+  do {                                                                                              \
+    const ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) throw CudaError(std::string("NCCL: ") + nccl().GetErrorString(r_) + " at " #call); \
+  } while (0)
+
+// Row sharding of one fit over `world` GPUs, one process per GPU (world == 0: not sharded).
+struct ShardInfo {
+  int rank = 0, world = 0;
+  ncclComm_t comm = nullptr;
+  unsigned char* peer[kMaxWorld] = {};  // peers' sweep sync blocks mapped by CUDA IPC (own: local)
+};
+
 }  // namespace rnmf_gpu
 
 using namespace rnmf_gpu;
 
 struct rnmf_gpu_context {
+  ShardInfo shard;
+  unsigned char* sync_block = nullptr;  // sweep-kernel sync block (kSweepSyncTotal bytes, own cudaMalloc)
   int device = 0;
   cudaStream_t stream = nullptr;
   int sm_count = 0;
@@ -254,10 +307,32 @@ static void check_problem_shapes(const rnmf_problem_shape& s, const char* who) {
 }
 
 // ==============================================================================================
+template <typename V>
+constexpr ncclDataType_t nccl_type() {
+  if constexpr (std::is_same<V, float>::value) return ncclFloat32;
+  else if constexpr (std::is_same<V, double>::value) return ncclFloat64;
+  else if constexpr (std::is_same<V, unsigned long long>::value) return ncclUint64;
+  else return ncclInt64;
+}
+
 template <typename T>
 class Engine {
  public:
   Engine(rnmf_gpu_context* ctx, Timer& tm) : ctx_(ctx), st_(ctx->stream), tm_(tm) {}
+
+  // ---- row sharding: this engine holds rows [row_off, row_off + m) of an m_total-row X --------
+  bool sharded() const { return ctx_->shard.world > 0; }
+  void set_rows(int64_t row_off, int64_t m_total) {
+    row_off_ = row_off;
+    m_total_ = m_total;
+  }
+  int64_t m_total() const { return sharded() ? m_total_ : m_; }
+  // in-place sum (or min / max) over the GPUs of a device buffer, on the engine's stream
+  template <typename V>
+  void allreduce(V* buf, size_t count, ncclRedOp_t op = ncclSum) {
+    if (!sharded() || count == 0) return;
+    RNMF_NCCL(nccl().AllReduce(buf, buf, count, nccl_type<V>(), op, ctx_->shard.comm, st_));
+  }
 
   // X for the X-streaming kernels: rows need a 16-byte aligned pitch (TMA, vector loads).  Device
   // input that already satisfies it is used in place (no copy); otherwise X is copied once into a
@@ -337,15 +412,26 @@ class Engine {
     auto* hb = ctx_->h<unsigned long long>("scan.bad.h", 2);
     auto* ho = ctx_->h<double>("scan.out.h", 2);
     RNMF_CUDA(cudaMemcpyAsync(hb, bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+    RNMF_CUDA(cudaStreamSynchronize(st_));
+    // positions as (row, column) of the whole matrix; sharded: the first offender over all GPUs
+    const int64_t nn = n_ > 0 ? n_ : 1;
+    for (int e = 0; e < 2; ++e)
+      if (hb[e] != ~0ull) hb[e] = (uint64_t(row_off_) + hb[e] / uint64_t(n)) * uint64_t(nn) + hb[e] % uint64_t(n);
+    if (sharded()) {
+      RNMF_CUDA(cudaMemcpyAsync(bad, hb, 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice, st_));
+      allreduce(bad, 2, ncclMin);
+      allreduce(out, 2);
+      RNMF_CUDA(cudaMemcpyAsync(hb, bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+    }
     RNMF_CUDA(cudaMemcpyAsync(ho, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st_));
     RNMF_CUDA(cudaStreamSynchronize(st_));
     if (hb[0] != ~0ull) {
       if (nonfinite_msg) throw DataError(nonfinite_msg);
-      const int64_t i = int64_t(hb[0]) / n, j = int64_t(hb[0]) % n;
+      const int64_t i = int64_t(hb[0]) / nn, j = int64_t(hb[0]) % nn;
       throw DataError("input contains non-finite entries at (" + std::to_string(i) + "," + std::to_string(j) + ")");
     }
     if (check_negative && hb[1] != ~0ull) {
-      const int64_t i = int64_t(hb[1]) / n, j = int64_t(hb[1]) % n;
+      const int64_t i = int64_t(hb[1]) / nn, j = int64_t(hb[1]) % nn;
       throw DataError("input contains negative entries at (" + std::to_string(i) + "," + std::to_string(j) + ")");
     }
     sum_ = ho[0];
@@ -413,13 +499,23 @@ class Engine {
     int* cqflag = ctx_->d<int>("cq.flag", 1);
     int* hflag = ctx_->h<int>("cq.flag.h", 1);
     // CholeskyQR2 first; Householder TSQR when A is too ill-conditioned (rank-deficient sketches)
-    auto qr = [&](const T* a, int64_t rows, T* out) {
+    // row-sharded Q (m x l): the Gram of every CholeskyQR pass is summed over the GPUs, and the
+    // fallback is shifted CholeskyQR3 (Gram-only, so it shards the same way); the n x l QR of the
+    // power iteration is replicated (identical input on every GPU).
+    const GramAllreduce gram_ar = [this](double* g, int64_t cnt) { allreduce(g, size_t(cnt)); };
+    auto qr = [&](const T* a, int64_t rows, T* out, bool row_sharded) {
       tm_.span(kQr, [&] {
-        tm_.launches += launch_cholqr2<T>(a, rows, l, out, cqws, cqflag, st_);
+        const GramAllreduce* ar = (row_sharded && sharded()) ? &gram_ar : nullptr;
+        tm_.launches += launch_cholqr2<T>(a, rows, l, out, cqws, cqflag, st_, ar);
         RNMF_CUDA(cudaMemcpyAsync(hflag, cqflag, sizeof(int), cudaMemcpyDeviceToHost, st_));
         RNMF_CUDA(cudaStreamSynchronize(st_));
         if (hflag[0] != 0) {
-          tm_.launches += launch_tsqr<T>(a, rows, l, out, ws, ctx_->max_smem, st_);
+          if (ar) {
+            const double shift = 11.0 * (double(m_total()) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
+            tm_.launches += launch_cholqr2<T>(a, rows, l, out, cqws, cqflag, st_, ar, shift);
+          } else {
+            tm_.launches += launch_tsqr<T>(a, rows, l, out, ws, ctx_->max_smem, st_);
+          }
           ++qr_fallbacks_;
         }
         ++qr_calls_;
@@ -427,13 +523,15 @@ class Engine {
     };
     xw(omega_dev, y);
     for (int64_t it = 0; it < q_iters; ++it) {
-      qr(y, m, qb);
+      qr(y, m, qb, true);
       xtw(qb, p, false);
-      qr(p, n, z);
+      allreduce(p, size_t(n) * l);  // X^T Q over all rows
+      qr(p, n, z, false);
       xw(z, y);
     }
-    qr(y, m, qb);
+    qr(y, m, qb, true);
     xtw(qb, b, true);
+    allreduce(b, size_t(l) * n);  // B = Q^T X over all rows
     *q_out = qb;
     *b_out = b;
   }
@@ -462,9 +560,11 @@ class Engine {
     const double wtx_bytes = double(g1) * double(n) * k * sizeof(T);
     const bool one_pass = fused_ok && wtx_bytes <= 0.25 * double(m) * double(n) * sizeof(T);
     x_passes_ = 2;
+    if (sharded() && !one_pass) throw ParameterError("B200 path: row-sharded metrics need the one-pass kernel (k <= 64)");
     tm_.span(kMetrics, [&] {
       tm_.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st_);
       tm_.launches += launch_gram_rows<T>(w, m, k, gpart2, wtw, st_);
+      allreduce(wtw, size_t(k) * k);  // W^T W over all rows (H H^T is replicated)
       int b1 = 0, b2 = 0;
       if (fused_ok) {
         T* wtx = one_pass ? ctx_->d<T>("met.wtx", size_t(g1) * n * k) : nullptr;
@@ -477,7 +577,15 @@ class Engine {
         ppgw = pw;
         if (one_pass) {
           double* pgh = ctx_->d<double>("met.ppgh2", size_t(grad_h_blocks(n, k)));
-          tm_.launches += launch_grad_h_reduce<T>(wtx, g1, n, k, h, wtw, pgh, &b2, st_);
+          if (sharded()) {
+            // W^T X: this GPU's CTA partials -> one n x k partial -> summed over the GPUs
+            T* wtx1 = ctx_->d<T>("met.wtx1", size_t(n) * k);
+            tm_.launches += launch_splitk_reduce<T>(wtx, g1, n, k, wtx1, false, st_);
+            allreduce(wtx1, size_t(n) * k);
+            tm_.launches += launch_grad_h_reduce<T>(wtx1, 1, n, k, h, wtw, pgh, &b2, st_);
+          } else {
+            tm_.launches += launch_grad_h_reduce<T>(wtx, g1, n, k, h, wtw, pgh, &b2, st_);
+          }
           ppgh = pgh;
           x_passes_ = 1;
         } else {
@@ -492,6 +600,11 @@ class Engine {
       }
       tm_.launches += launch_sum_parts(pobj, b1, res, st_);
       tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
+      if (sharded()) {
+        // objective and the grad_W term are sums over rows: add the GPUs' values (grad_H is replicated)
+        allreduce(res, 1);
+        allreduce(tmp, 1);
+      }
       tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
       // res[1] = pgw + pgh, done on device by a 2-element sum
       tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
@@ -513,6 +626,7 @@ class Engine {
   double sum_ = 0.0, sumsq_ = 0.0;
   const T* x_ = nullptr;
   int64_t m_ = 0, n_ = 0, ldx_ = 0;
+  int64_t row_off_ = 0, m_total_ = 0;
   int x_passes_ = 2;
 };
 
@@ -567,9 +681,23 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   a.trace_pgrad = ctx->d<double>("sw.tpgrad", size_t(max_iter + 1));
   a.trace_time = ctx->d<unsigned long long>("sw.ttime", size_t(max_iter + 1));
   a.status = ctx->d<long long>("sw.status", 2);
-  a.barrier = reinterpret_cast<unsigned*>(ctx->d<unsigned long long>("sw.sync", kSweepSyncBytes / 8));
+  a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+  if (eng.sharded()) {
+    // row-sharded: column steps and W-side sums run over every CTA of every GPU
+    a.world = ctx->shard.world;
+    a.rank = ctx->shard.rank;
+    for (int p = 0; p < a.world; ++p) a.peer_sync[p] = ctx->shard.peer[p];
+    long long* gs = ctx->d<long long>("sw.gsum", 1);
+    long long* hgs = ctx->h<long long>("sw.gsum.h", 1);
+    hgs[0] = plan.grid;
+    RNMF_CUDA(cudaMemcpyAsync(gs, hgs, sizeof(long long), cudaMemcpyHostToDevice, st));
+    eng.allreduce(gs, 1);
+    RNMF_CUDA(cudaMemcpyAsync(hgs, gs, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaStreamSynchronize(st));
+    a.xtotal = hgs[0];
+  }
   // RNMF_PROF=1: per-phase cycle counters of CTA 0, printed to stderr (development aid)
   const bool prof = std::getenv("RNMF_PROF") != nullptr && sweep_prof_compiled();
   if (std::getenv("RNMF_PROF") != nullptr && !prof)
@@ -687,28 +815,33 @@ static void fill_gaussian(Rng& rng, double* out, size_t count) {
   for (size_t i = 0; i < count; ++i) out[i] = rng.gaussian();
 }
 
+// fit_impl: rhals_fit (fit = true) or compress (fit = false).  Row-sharded contexts hold rows
+// [row_off, row_off + m) of an m_total-row X (m_total < 0: not sharded, m_total = m).
 template <typename T>
 static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int64_t m, int64_t n,
                      const rnmf_solver_options& o, const double* omega, const double* w0, const double* h0,
                      void* w_out, void* h_out, rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len,
-                     void* q_out, void* b_out, void* wt_out, int64_t* l_out, bool fit) {
+                     void* q_out, void* b_out, void* wt_out, int64_t* l_out, bool fit, int64_t row_off = 0,
+                     int64_t m_total = -1) {
   const auto t0 = std::chrono::steady_clock::now();
   ctx->last = rnmf_stage_times{};
   Timer tm(ctx);
   Engine<T> eng(ctx, tm);
   if (m < 0 || n < 0) throw ShapeError("X has negative dimensions " + shape_string(m, n));
+  const int64_t mt = m_total < 0 ? m : m_total;
+  eng.set_rows(row_off, mt);
   const T* x = nullptr;
-  if (m * n > 0) {
-    x = eng.import_x(x_in, location, m, n);
+  if (mt * n > 0) {
+    if (m * n > 0) x = eng.import_x(x_in, location, m, n);
     eng.scan(true, nullptr);
   }
-  validate_options_after_data(m, n, o);
+  validate_options_after_data(mt, n, o);
   check_supported(o);
   if (fit && trace_cap < o.max_iter + 1)
     throw ParameterError("trace buffer too small: need " + std::to_string(o.max_iter + 1) + " records, have " +
                          std::to_string(trace_cap));
   const int k = int(o.rank);
-  const int64_t l64 = sketch_width(m, n, o.rank, o.oversampling, o.power_iterations);
+  const int64_t l64 = sketch_width(mt, n, o.rank, o.oversampling, o.power_iterations);
   const int l = int(l64);
   if (l > tsqr_max_l(ctx->max_smem) || l > 128)
     throw ParameterError("B200 path: sketch width " + std::to_string(l) + " above the supported maximum " +
@@ -737,10 +870,14 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
       return;
     }
     Rng rng(o.seed);
-    if (w0)
+    if (w0) {
       std::memcpy(uw, w0, sizeof(double) * size_t(m) * k);
-    else
+    } else {
+      // the reference draws all m_total x k entries of W, then H: this GPU keeps its rows
+      for (int64_t i = 0; i < row_off * k; ++i) rng.uniform();
       fill_uniform(rng, uw, size_t(m) * k);
+      for (int64_t i = (row_off + m) * k; i < mt * k; ++i) rng.uniform();
+    }
     if (h0)
       std::memcpy(uh, h0, sizeof(double) * size_t(k) * n);
     else
@@ -755,7 +892,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   }
   drawer.join();
 
-  const double scale = std::sqrt(eng.sum() / double(m * n) / double(k));
+  const double scale = std::sqrt(eng.sum() / double(mt * n) / double(k));
   T* w = ctx->d<T>("w", size_t(m) * k);
   T* h = ctx->d<T>("h", size_t(k) * n);
   double* uw_d = ctx->d<double>("init.uw.d", size_t(m) * k);
@@ -799,7 +936,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
     a.trace_pgrad = ctx->d<double>("sw.tpgrad", 1);
     a.trace_time = ctx->d<unsigned long long>("sw.ttime", 1);
     a.status = ctx->d<long long>("sw.status", 2);
-    a.barrier = reinterpret_cast<unsigned*>(ctx->d<unsigned long long>("sw.sync", kSweepSyncBytes / 8));
+    a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
     const int64_t plen = sweep_part_len(l, k);
     a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
     a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
@@ -914,7 +1051,7 @@ static void stage_impl(rnmf_gpu_context* ctx, int location, const rnmf_problem_s
   a.trace_pgrad = ctx->d<double>("sw.tpgrad", 2);
   a.trace_time = ctx->d<unsigned long long>("sw.ttime", 2);
   a.status = ctx->d<long long>("sw.status", 2);
-  a.barrier = reinterpret_cast<unsigned*>(ctx->d<unsigned long long>("sw.sync", kSweepSyncBytes / 8));
+  a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
   const int64_t plen = sweep_part_len(l, k);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
@@ -1090,8 +1227,64 @@ int rnmf_gpu_context_create(int device, rnmf_gpu_context** out, char* err, size_
     ctx->sm_count = prop.multiProcessorCount;
     ctx->max_smem = int(prop.sharedMemPerBlockOptin);
     RNMF_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    RNMF_CUDA(cudaMalloc(&ctx->sync_block, kSweepSyncTotal));
     *out = ctx.release();
   });
+}
+
+int rnmf_gpu_comm_unique_id(unsigned char* id_out, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    if (!id_out) throw rnmf_gpu::ParameterError("null id buffer");
+    static_assert(sizeof(ncclUniqueId) == RNMF_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId id;
+    RNMF_NCCL(nccl().GetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof id);
+  });
+}
+
+int rnmf_gpu_context_create_sharded(int device, int rank, int world, const unsigned char* id,
+                                    rnmf_gpu_context** out, char* err, size_t err_cap) {
+  const int st = rnmf_gpu_context_create(device, out, err, err_cap);
+  if (st != RNMF_OK) return st;
+  rnmf_gpu_context* ctx = *out;
+  const int st2 = guarded(err, err_cap, [&] {
+    if (!id) throw rnmf_gpu::ParameterError("null communicator id");
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+      throw rnmf_gpu::ParameterError("sharded context: need 0 <= rank < world <= " + std::to_string(kMaxWorld));
+    DeviceGuard g(device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    RNMF_NCCL(nccl().CommInitRank(&ctx->shard.comm, world, uid, rank));
+    ctx->shard.rank = rank;
+    ctx->shard.world = world;
+    // map every peer's sweep sync block (CUDA IPC over NVLink); own block stays local
+    cudaIpcMemHandle_t mine;
+    RNMF_CUDA(cudaIpcGetMemHandle(&mine, ctx->sync_block));
+    unsigned char* dh = nullptr;
+    RNMF_CUDA(cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * (world + 1)));
+    RNMF_CUDA(cudaMemcpyAsync(dh + sizeof(cudaIpcMemHandle_t) * world, &mine, sizeof mine, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    RNMF_NCCL(nccl().AllGather(dh + sizeof(cudaIpcMemHandle_t) * world, dh, sizeof(cudaIpcMemHandle_t), ncclUint8,
+                               ctx->shard.comm, ctx->stream));
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(world));
+    RNMF_CUDA(cudaMemcpyAsync(all.data(), dh, sizeof(cudaIpcMemHandle_t) * world, cudaMemcpyDeviceToHost, ctx->stream));
+    RNMF_CUDA(cudaStreamSynchronize(ctx->stream));
+    RNMF_CUDA(cudaFree(dh));
+    for (int p = 0; p < world; ++p) {
+      if (p == rank) {
+        ctx->shard.peer[p] = ctx->sync_block;
+      } else {
+        void* ptr = nullptr;
+        RNMF_CUDA(cudaIpcOpenMemHandle(&ptr, all[size_t(p)], cudaIpcMemLazyEnablePeerAccess));
+        ctx->shard.peer[p] = static_cast<unsigned char*>(ptr);
+      }
+    }
+  });
+  if (st2 != RNMF_OK) {
+    rnmf_gpu_context_destroy(ctx);
+    *out = nullptr;
+  }
+  return st2;
 }
 
 void rnmf_gpu_context_destroy(rnmf_gpu_context* ctx) {
@@ -1105,6 +1298,10 @@ void rnmf_gpu_context_destroy(rnmf_gpu_context* ctx) {
   for (auto& kv : ctx->pinned)
     if (kv.second.p) cudaFreeHost(kv.second.p);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  for (int p = 0; p < ctx->shard.world; ++p)
+    if (p != ctx->shard.rank && ctx->shard.peer[p]) cudaIpcCloseMemHandle(ctx->shard.peer[p]);
+  if (ctx->shard.comm) nccl().CommDestroy(ctx->shard.comm);
+  if (ctx->sync_block) cudaFree(ctx->sync_block);
   cudaStreamDestroy(ctx->stream);
   if (prev >= 0) cudaSetDevice(prev);
   delete ctx;
@@ -1131,6 +1328,29 @@ int rnmf_gpu_rhals_fit(rnmf_gpu_context* ctx, const void* x, int dtype, int loca
     else
       fit_impl<double>(ctx, x, location, m, n, *opts, omega, w0, h0, w_out, h_out, trace, trace_cap, trace_len,
                        nullptr, nullptr, nullptr, nullptr, true);
+  });
+}
+
+int rnmf_gpu_rhals_fit_sharded(rnmf_gpu_context* ctx, const void* x_local, int dtype, int location,
+                               int64_t m_local, int64_t row_offset, int64_t m_total, int64_t n,
+                               const rnmf_solver_options* opts, const double* omega, const double* w0_local,
+                               const double* h0, void* w_out, void* h_out, rnmf_trace_record* trace,
+                               int64_t trace_cap, int64_t* trace_len, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!opts || !trace || !trace_len) throw rnmf_gpu::ParameterError("null options / trace pointer");
+    if (ctx->shard.world < 1) throw rnmf_gpu::ParameterError("context is not sharded (rnmf_gpu_context_create_sharded)");
+    if (m_local < 1 || row_offset < 0 || m_total < row_offset + m_local || n < 0)
+      throw rnmf_gpu::ShapeError("sharded X: rows [" + std::to_string(row_offset) + ", " +
+                                 std::to_string(row_offset + m_local) + ") of " + std::to_string(m_total));
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      fit_impl<float>(ctx, x_local, location, m_local, n, *opts, omega, w0_local, h0, w_out, h_out, trace, trace_cap,
+                      trace_len, nullptr, nullptr, nullptr, nullptr, true, row_offset, m_total);
+    else
+      fit_impl<double>(ctx, x_local, location, m_local, n, *opts, omega, w0_local, h0, w_out, h_out, trace,
+                       trace_cap, trace_len, nullptr, nullptr, nullptr, nullptr, true, row_offset, m_total);
   });
 }
 
