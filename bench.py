@@ -8,8 +8,9 @@ W, H and the trace inside every step).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
-N > 1 (torchrun): the path is run as N independent replicas, one per GPU (weak scaling); the
-row-sharded multi-GPU fit is not implemented yet.
+N > 1 (torchrun, one process per GPU): ONE fit of the config with X sharded by rows over the N
+GPUs (paper_1711_02037_b200.distributed; strong scaling); `value` = sweeps/s of that fit, device
+time max over ranks.
 """
 from __future__ import annotations
 
@@ -210,6 +211,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--math", default="exact", choices=["exact", "tf32x3", "tf32"])
+    ap.add_argument("--sharded", action="store_true", help="row-sharded path even at N = 1 (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
@@ -231,8 +233,25 @@ def main():
 
     cfg, xd, omega, w0, h0, opts = make_workload(args.config, device)
     opts.math_mode = {"exact": api.MathMode.Exact, "tf32x3": api.MathMode.TF32x3, "tf32": api.MathMode.TF32}[args.math]
-    ctx = api.Context(local)
     esz = xd.element_size()
+    m_total = cfg.m
+    if world > 1 or args.sharded:
+        from paper_1711_02037_b200 import distributed as pdist
+
+        ctx = (pdist.ShardedContext(local) if world > 1 else
+               pdist.ShardedContext(local, rank=0, world=1, comm_id=pdist.comm_unique_id()))
+        off, cnt = pdist.shard_rows(m_total, world, rank)
+        xd = xd[off:off + cnt].contiguous()
+        w0 = np.ascontiguousarray(w0[off:off + cnt])
+
+        def fit(x):
+            return pdist.rhals_fit_sharded(x, opts, row_offset=off, m_total=m_total, ctx=ctx, omega=omega, w0=w0,
+                                           h0=h0)
+    else:
+        ctx = api.Context(local)
+
+        def fit(x):
+            return api.rhals_fit(x, opts, omega=omega, w0=w0, h0=h0, ctx=ctx)
 
     def barrier():
         if world > 1:
@@ -241,7 +260,11 @@ def main():
 
     # ---- device-resident X: `value`
     for _ in range(args.warmup):
-        api.rhals_fit(xd, opts, omega=omega, w0=w0, h0=h0, ctx=ctx)
+        fit(xd)
+    # X per GPU below 2x the 126 MB L2 (sharded / small configs): flush L2 between steps so no
+    # step starts with X cached by the previous one (the library's device time excludes the flush)
+    x_bytes_local = xd.numel() * esz
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device) if x_bytes_local < 252e6 else None
     sampler = ClockSampler(local)
     barrier()
     sampler.start()
@@ -249,7 +272,9 @@ def main():
     dev_ms, launches, stages = [], 0, []
     last = None
     for _ in range(args.steps):
-        last = api.rhals_fit(xd, opts, omega=omega, w0=w0, h0=h0, ctx=ctx)
+        if flush is not None:
+            flush.zero_()
+        last = fit(xd)
         st = ctx.stage_times()
         dev_ms.append(st["total_ms"])
         launches += int(st["kernel_launches"])
@@ -264,20 +289,20 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     sweeps = last.trace[-1].iter
-    value = world * sweeps * args.steps / (total_ms / 1e3)
+    value = sweeps * args.steps / (total_ms / 1e3)  # one fit over all N GPUs
 
     # ---- e2e through the public API with host X (pinned)
     x_pin = torch.empty(xd.shape, dtype=xd.dtype, pin_memory=True)
     x_pin.copy_(xd)
     x_np = x_pin.numpy()
     for _ in range(1):
-        api.rhals_fit(x_np, opts, omega=omega, w0=w0, h0=h0, ctx=ctx)
+        fit(x_np)
     barrier()
     e2e_ms = []
     for _ in range(args.steps):
         ev0 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
-        res = api.rhals_fit(x_np, opts, omega=omega, w0=w0, h0=h0, ctx=ctx)
+        res = fit(x_np)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         _ = res.trace[-1].rel_err  # the step's result is on the host
     barrier()
@@ -286,11 +311,28 @@ def main():
         t = torch.tensor([e2e_total], device=device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_value = world * sweeps * args.steps / (e2e_total / 1e3)
-    m, n, k = cfg.m, cfg.n, cfg.k
+    e2e_value = sweeps * args.steps / (e2e_total / 1e3)
+    m, n, k = xd.shape[0], cfg.n, cfg.k
     l = min(cfg.k + cfg.p, m, n)
-    h2d = m * n * esz + 8 * (n * l + m * k + k * n)
-    d2h = esz * (m * k + k * n) + 56 * (sweeps + 1)
+    # whole job: every rank copies its X rows and W0 rows, Omega / H0 replicated; W rows + H back
+    h2d = cfg.m * n * esz + 8 * cfg.m * k + world * 8 * (n * l + k * n)
+    d2h = esz * (cfg.m * k + world * k * n) + world * 56 * (sweeps + 1)
+
+    # tensor-core sketch (math_mode TF32X3, a performance mode: the verification runs use EXACT):
+    # the same X passes once more for the sketch roofline, outside the timed region
+    tc_sketch = None
+    if esz == 4 and world == 1 and args.math == "exact":
+        opts.math_mode = api.MathMode.TF32x3
+        for _ in range(2):
+            fit(xd)
+        tst = ctx.stage_times()
+        opts.math_mode = api.MathMode.Exact
+        tb = tst["xw_bytes"] + tst["xtw_bytes"]
+        tms = tst["xw_ms"] + tst["xtw_ms"]
+        tc_sketch = {"math_mode": "tf32x3", "sketch_gbs": tb / (tms / 1e3) / 1e9 if tms > 0 else None,
+                     "xw_gbs": tst["xw_bytes"] / (tst["xw_ms"] / 1e3) / 1e9 if tst["xw_ms"] > 0 else None,
+                     "xtw_gbs": tst["xtw_bytes"] / (tst["xtw_ms"] / 1e3) / 1e9 if tst["xtw_ms"] > 0 else None,
+                     "fit_ms": tst["total_ms"]}
 
     if rank != 0:
         if world > 1:
@@ -318,14 +360,15 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32" if esz == 4 else "f64",
         "data": "synthetic (seeded stand-in for the paper's dataset; see paper_1711_02037_b200/workloads.py)",
-        "config": {"workload": cfg.name, "m": m, "n": n, "k": k, "p": cfg.p, "q": cfg.q, "iters": cfg.iters,
+        "config": {"workload": cfg.name, "m": cfg.m, "n": n, "k": k, "p": cfg.p, "q": cfg.q, "iters": cfg.iters,
                    "tol": 1e-300, "math_mode": args.math,
-                   "parallelism": "replicas" if world > 1 else "single-gpu",
-                   "l2": f"X = {m * n * esz / 1e6:.0f} MB > 126 MB L2 (no flush needed)"},
+                   "parallelism": f"rows{world}" if world > 1 else "single-gpu",
+                   "l2": (f"X per GPU = {m * n * esz / 1e6:.0f} MB > 126 MB L2 (no flush needed)" if flush is None
+                          else f"X per GPU = {m * n * esz / 1e6:.0f} MB: L2 flushed (256 MB write) between steps")},
         "end_to_end_s": ms_per_step / 1e3,
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_total / args.steps},
@@ -341,6 +384,8 @@ def main():
                                     "metrics_pass_gbs": met_gbs,
                                     "metrics_bytes_per_eval": agg["metrics_bytes"] / max(agg["metrics_passes"], 1),
                                     "ncu_dram_bytes_per_launch": traffic.get("kernels") if traffic else None}},
+        "roofline_tensor_core_sketch": (dict(tc_sketch, frac=tc_sketch["sketch_gbs"] / hbm_peak, peak=hbm_peak)
+                                        if tc_sketch and tc_sketch["sketch_gbs"] else None),
         "stage_ms": {key: agg[key] for key in ("scan_ms", "sketch_ms", "qr_ms", "init_ms", "sweeps_ms", "metrics_ms",
                                                "xw_ms", "xtw_ms", "h2d_ms", "d2h_ms", "total_ms")},
         "stage_share": shares,
