@@ -19,49 +19,79 @@ namespace rnmf_gpu {
 namespace {
 
 constexpr int kCqThreads = 256;
-constexpr int kGramRows = 32;      // rows staged per chunk
-constexpr int kGramMaxAcc = 64;    // l <= 128: l*l/256 entries per thread
 
+// part[b] = A[rows of b]^T A[rows of b] (l x l, fp64), rows split evenly over the CTAs.  Rows are
+// staged 64 at a time in fp64 shared memory; thread (row group rg, block pair (ba <= bb)) owns a
+// 4 x 4 block of the upper triangle and accumulates it over the rows rg, rg + RG, ... of each
+// chunk (16 FMAs per 8 shared loads); the RG row-group partials are combined in fixed order and
+// the block is written to both triangles.
+constexpr int kGramChunkRows = 64;
 template <typename T>
 __global__ void __launch_bounds__(kCqThreads) cq_gram_kernel(const T* __restrict__ A, int64_t rows, int l,
                                                              double* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* tile = reinterpret_cast<double*>(smem);  // [kGramRows][l]
+  const int lp = ((l + 3) / 4) * 4 + 1;             // padded row stride (odd: spreads banks)
+  double* tile = reinterpret_cast<double*>(smem);    // [kGramChunkRows][lp]
+  double* red = tile + kGramChunkRows * lp;          // [RG][npairs][16]
+  const int nbk = (l + 3) / 4, npairs = nbk * (nbk + 1) / 2;
+  const int RG = max(1, min(4, kCqThreads / npairs));
   const int64_t r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
-  const int ll = l * l;
-  const int nacc = (ll + kCqThreads - 1) / kCqThreads;
-  double acc[kGramMaxAcc];
-#pragma unroll
-  for (int u = 0; u < kGramMaxAcc; ++u) acc[u] = 0.0;
-  for (int64_t base = r0; base < r1; base += kGramRows) {
-    const int nr = int(r1 - base < kGramRows ? r1 - base : kGramRows);
-    __syncthreads();
-    for (int e = threadIdx.x; e < kGramRows * l; e += kCqThreads) {
-      const int rr = e / l;
-      tile[e] = rr < nr ? double(A[(base + rr) * l + e % l]) : 0.0;
+  for (int pr0 = 0; pr0 < npairs; pr0 += kCqThreads / RG) {
+    const int slot = threadIdx.x % (kCqThreads / RG), rg = threadIdx.x / (kCqThreads / RG);
+    const int pr = pr0 + slot;
+    int ba = 0, bb = 0;
+    if (pr < npairs) {  // pair index -> (ba, bb), ba <= bb, row-major over the upper triangle
+      int rem = pr;
+      while (rem >= nbk - ba) {
+        rem -= nbk - ba;
+        ++ba;
+      }
+      bb = ba + rem;
     }
-    __syncthreads();
+    double acc[4][4];
 #pragma unroll
-    for (int u = 0; u < kGramMaxAcc; ++u) {
-      if (u < nacc) {
-        const int e = threadIdx.x + kCqThreads * u;
-        if (e < ll) {
-          const int a = e / l, b = e % l;
-          double s0 = 0.0, s1 = 0.0;
-          for (int r = 0; r < kGramRows; r += 2) {
-            s0 += tile[r * l + a] * tile[r * l + b];
-            s1 += tile[(r + 1) * l + a] * tile[(r + 1) * l + b];
-          }
-          acc[u] += s0 + s1;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int64_t base = r0; base < r1; base += kGramChunkRows) {
+      const int nr = int(r1 - base < kGramChunkRows ? r1 - base : kGramChunkRows);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kGramChunkRows * lp; e += kCqThreads) {
+        const int rr = e / lp, cc = e % lp;
+        tile[e] = (rr < nr && cc < l) ? double(A[(base + rr) * l + cc]) : 0.0;
+      }
+      __syncthreads();
+      if (pr < npairs && rg < RG) {
+        for (int rr = rg; rr < nr; rr += RG) {
+          const double* tr = tile + rr * lp;
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = tr[4 * ba + i], b[i] = tr[4 * bb + i];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
       }
     }
-  }
+    __syncthreads();
+    if (pr < npairs && rg < RG)
 #pragma unroll
-  for (int u = 0; u < kGramMaxAcc; ++u) {
-    if (u < nacc) {
-      const int e = threadIdx.x + kCqThreads * u;
-      if (e < ll) part[int64_t(blockIdx.x) * ll + e] = acc[u];
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[(rg * (kCqThreads / RG) + slot) * 16 + i * 4 + j] = acc[i][j];
+    __syncthreads();
+    if (rg == 0 && pr < npairs) {
+      const int64_t ll = int64_t(l) * l;
+      for (int q = 0; q < 16; ++q) {
+        double v = 0.0;
+        for (int g2 = 0; g2 < RG; ++g2) v += red[(g2 * (kCqThreads / RG) + slot) * 16 + q];
+        const int a = 4 * ba + q / 4, b = 4 * bb + q % 4;
+        if (a < l && b < l) {
+          part[int64_t(blockIdx.x) * ll + int64_t(a) * l + b] = v;
+          part[int64_t(blockIdx.x) * ll + int64_t(b) * l + a] = v;
+        }
+      }
     }
   }
 }
@@ -199,7 +229,8 @@ int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* f
   double* rinv1 = part + int64_t(nb) * l * l;
   double* rinv2 = rinv1 + int64_t(l) * l;
   double* q1 = rinv2 + int64_t(l) * l;  // rows x l, fp64 intermediate
-  const size_t gsm = size_t(kGramRows) * l * sizeof(double);
+  const int lpad = ((l + 3) / 4) * 4 + 1;
+  const size_t gsm = (size_t(kGramChunkRows) * lpad + size_t(kCqThreads) * 16) * sizeof(double);
   const size_t csm = size_t(2) * l * (l + 1) * sizeof(double);
   const size_t asm_ = size_t(l) * (l + 1) * sizeof(double) + size_t(64) * (l + 1) * sizeof(double);
   RNMF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream));
@@ -218,13 +249,10 @@ int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* f
     cq_gram_kernel<std::remove_const_t<std::remove_pointer_t<decltype(src)>>><<<nb, kCqThreads, gsm, stream>>>(
         src, rows, l, part);
     RNMF_CUDA_LAUNCH();
-    int np = nb;
-    if (allreduce) {
-      launches += launch_reduce_parts(part, nb, l * l, part + int64_t(nb) * 0, stream);  // in place: part[0]
-      (*allreduce)(part, int64_t(l) * l);
-      np = 1;
-    }
-    cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, np, l, rinv, flag, check_identity, shift);
+    // the CTA partials summed by a multi-block fixed-order reduction (in place into part[0])
+    launches += launch_reduce_parts(part, nb, l * l, part, stream);
+    if (allreduce) (*allreduce)(part, int64_t(l) * l);
+    cq_chol_kernel<<<1, kCqThreads, csm, stream>>>(part, 1, l, rinv, flag, check_identity, shift);
     RNMF_CUDA_LAUNCH();
     launches += 2;
   };
