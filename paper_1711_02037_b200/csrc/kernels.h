@@ -134,6 +134,21 @@ template <typename T>
 int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream,
                    const GramAllreduce* allreduce = nullptr, double shift_rel = 0.0);
 
+// ---- NNDSVD init (kernels_nndsvd.cu) ------------------------------------------------------------
+// eigen-decomposition of a symmetric l x l fp64 matrix (l <= 64): eval descending, evec columns
+int launch_jacobi_eig(const double* g, int l, double* eval, double* evec, cudaStream_t stream);
+int nndsvd_norm_blocks(int64_t rows);
+// part[b][j][2] = block partial sums of squares of the positive / negative parts of column j of
+// u = S U(:, :k) diag(colscale) (S rows x l, or l x rows when `transpose`); U is l x l.
+template <typename T>
+int launch_nndsvd_norms(const T* s, int64_t rows, int l, bool transpose, const double* u, int k,
+                        const double* colscale, double* part, cudaStream_t stream);
+// out = coef-weighted positive / negative part of u, zeros -> fill (rows x k, or k x rows)
+template <typename T>
+int launch_nndsvd_apply(const T* s, int64_t rows, int l, bool transpose, const double* u, int k,
+                        const double* colscale, const double* coef, double fill, T* out, bool out_transposed,
+                        cudaStream_t stream);
+
 // ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cu) -----------------------------
 enum SweepFlags : int {
   kInitWt = 1,    // W~ <- Q^T W

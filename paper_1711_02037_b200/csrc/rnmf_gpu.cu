@@ -270,8 +270,7 @@ static void validate_options_after_data(int64_t m, int64_t n, const rnmf_solver_
 }
 
 static void check_supported(const rnmf_solver_options& o) {
-  if (o.init != RNMF_INIT_RANDOM)
-    throw ParameterError("B200 path: InitScheme::Svd is not implemented yet (use Random or pass w0/h0)");
+  if (o.init != RNMF_INIT_RANDOM && o.init != RNMF_INIT_SVD) throw ParameterError("unknown InitScheme");
   if (o.order != RNMF_ORDER_GROUPED)
     throw ParameterError("B200 path: only UpdateOrder::Grouped is implemented");
   if (o.reseed_dead) throw ParameterError("B200 path: reseed_dead is not implemented");
@@ -815,6 +814,91 @@ static void fill_gaussian(Rng& rng, double* out, size_t count) {
   for (size_t i = 0; i < count; ++i) out[i] = rng.gaussian();
 }
 
+// InitScheme::Svd, nndsvd_init (p/src/hals.cpp:126-170): a second rqb with its own stream
+// (seed = the init Rng's first next_u64, uniform test matrix, p = min(20, min(m,n) - k), q = 2), the
+// SVD of its B through the Jacobi eigen-decomposition of B B^T, and the NNDSVD split of the leading
+// k pairs into w (this GPU's rows) and h; zeros become mean(X)/100.  Runs before the fit's own rqb
+// (the two sketches are independent; the rqb buffers are reused).
+template <typename T>
+static void nndsvd_init_dev(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnmf_solver_options& o, int64_t m,
+                            int64_t n, int64_t mt, T* w, T* h) {
+  cudaStream_t st = ctx->stream;
+  const int k = int(o.rank);
+  const int64_t p2 = std::min<int64_t>(20, std::min(mt, n) - k);
+  const int l2 = int(sketch_width(mt, n, k, p2, 2));
+  if (l2 > 64) throw ParameterError("B200 path: InitScheme::Svd supports a sketch width up to 64");
+  Rng init_rng(o.seed);
+  Rng orng(init_rng.next_u64());
+  std::vector<double> om(size_t(n) * l2);
+  fill_uniform(orng, om.data(), om.size());
+  T* om_dev = eng.upload_converted("omega.svd", om.data(), om.size());
+  T *q2 = nullptr, *b2 = nullptr;
+  tm.span(kSketch, [&] { eng.rqb(l2, 2, om_dev, RNMF_MATH_EXACT, &q2, &b2); });
+  tm.span(kInit, [&] {
+    double* gpart = ctx->d<double>("svd.gpart", size_t(gram_parts(n)) * l2 * l2);
+    double* g = ctx->d<double>("svd.g", size_t(l2) * l2);
+    double* eval = ctx->d<double>("svd.eval", size_t(l2));
+    double* evec = ctx->d<double>("svd.evec", size_t(l2) * l2);
+    tm.launches += launch_gram_cols<T>(b2, l2, n, gpart, g, st);
+    tm.launches += launch_jacobi_eig(g, l2, eval, evec, st);
+    double* heval = ctx->h<double>("svd.eval.h", size_t(l2));
+    RNMF_CUDA(cudaMemcpyAsync(heval, eval, sizeof(double) * l2, cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> sv(static_cast<size_t>(k));
+    for (int j = 0; j < k; ++j) sv[size_t(j)] = std::sqrt(std::max(heval[j], 0.0));
+    // u = Q U(:, :k); v = B^T U(:, :k) / s
+    double* hcs = ctx->h<double>("svd.cs.h", size_t(2) * k);
+    for (int j = 0; j < k; ++j) {
+      hcs[j] = 1.0;
+      hcs[k + j] = sv[size_t(j)] > 0.0 ? 1.0 / sv[size_t(j)] : 0.0;
+    }
+    double* cs = ctx->d<double>("svd.cs", size_t(2) * k);
+    RNMF_CUDA(cudaMemcpyAsync(cs, hcs, sizeof(double) * 2 * k, cudaMemcpyHostToDevice, st));
+    const int bu = nndsvd_norm_blocks(m), bv = nndsvd_norm_blocks(n);
+    double* pu = ctx->d<double>("svd.pu", size_t(bu) * 2 * k);
+    double* pv = ctx->d<double>("svd.pv", size_t(bv) * 2 * k);
+    double* nrm = ctx->d<double>("svd.nrm", size_t(4) * k);
+    tm.launches += launch_nndsvd_norms<T>(q2, m, l2, false, evec, k, cs, pu, st);
+    tm.launches += launch_nndsvd_norms<T>(b2, n, l2, true, evec, k, cs + k, pv, st);
+    tm.launches += launch_reduce_parts(pu, bu, 2 * k, nrm, st);
+    tm.launches += launch_reduce_parts(pv, bv, 2 * k, nrm + 2 * k, st);
+    eng.allreduce(nrm, size_t(2) * k);  // sharded: u's rows are spread over the GPUs
+    double* hn = ctx->h<double>("svd.nrm.h", size_t(4) * k);
+    RNMF_CUDA(cudaMemcpyAsync(hn, nrm, sizeof(double) * 4 * k, cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaStreamSynchronize(st));
+    // coefficients of the positive / negative parts (p/src/hals.cpp:145-160)
+    double* hc = ctx->h<double>("svd.coef.h", size_t(4) * k);
+    for (int j = 0; j < k; ++j) {
+      double* cu = hc + 2 * j;
+      double* cv = hc + 2 * k + 2 * j;
+      cu[0] = cu[1] = cv[0] = cv[1] = 0.0;
+      if (j == 0) {  // leading pair with the signs folded away: sqrt(s0) |u0|, sqrt(s0) |v0|
+        cu[0] = cu[1] = cv[0] = cv[1] = std::sqrt(sv[0]);
+        continue;
+      }
+      const double nup = std::sqrt(hn[2 * j]), nun = std::sqrt(hn[2 * j + 1]);
+      const double nvp = std::sqrt(hn[2 * k + 2 * j]), nvn = std::sqrt(hn[2 * k + 2 * j + 1]);
+      const double mp = nup * nvp, mn = nun * nvn;
+      if (std::max(mp, mn) <= 0.0) continue;  // degenerate pair: left for the fill
+      const bool pos = mp >= mn;
+      const double scale = std::sqrt(sv[size_t(j)] * std::max(mp, mn));
+      if (pos) {
+        cu[0] = scale / nup;
+        cv[0] = scale / nvp;
+      } else {
+        cu[1] = scale / nun;
+        cv[1] = scale / nvn;
+      }
+    }
+    double* coef = ctx->d<double>("svd.coef", size_t(4) * k);
+    RNMF_CUDA(cudaMemcpyAsync(coef, hc, sizeof(double) * 4 * k, cudaMemcpyHostToDevice, st));
+    const double fill = eng.sum() / double(mt * n) / 100.0;
+    tm.launches += launch_nndsvd_apply<T>(q2, m, l2, false, evec, k, cs, coef, fill, w, false, st);
+    tm.launches += launch_nndsvd_apply<T>(b2, n, l2, true, evec, k, cs + k, coef + 2 * k, fill, h, true, st);
+    RNMF_CUDA(cudaStreamSynchronize(st));  // host coefficient buffers are reused by later calls
+  });
+}
+
 // fit_impl: rhals_fit (fit = true) or compress (fit = false).  Row-sharded contexts hold rows
 // [row_off, row_off + m) of an m_total-row X (m_total < 0: not sharded, m_total = m).
 template <typename T>
@@ -860,10 +944,18 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   }
   T* om_dev = eng.upload_converted("omega", om, size_t(n) * l);
 
+  const bool svd_init = o.init == RNMF_INIT_SVD;
+  if (svd_init && (w0 || h0)) throw ParameterError("init overrides require InitScheme::Random");
+  if (svd_init && (m * n == 0 || k < 1)) throw ParameterError("InitScheme::Svd needs a non-empty X");
+  T* w = ctx->d<T>("w", size_t(m) * k);
+  T* h = ctx->d<T>("h", size_t(k) * n);
+  if (svd_init) nndsvd_init_dev<T>(ctx, eng, tm, o, m, n, mt, w, h);
+
   // initial draws on a host thread while the GPU sketches (random_init, p/src/hals.cpp:118-124)
   double* uw = ctx->h<double>("init.uw", size_t(m) * k);
   double* uh = ctx->h<double>("init.uh", size_t(k) * n);
   std::thread drawer([&] {
+    if (svd_init) return;
     if (w0 && h0) {
       std::memcpy(uw, w0, sizeof(double) * size_t(m) * k);
       std::memcpy(uh, h0, sizeof(double) * size_t(k) * n);
@@ -893,18 +985,18 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   drawer.join();
 
   const double scale = std::sqrt(eng.sum() / double(mt * n) / double(k));
-  T* w = ctx->d<T>("w", size_t(m) * k);
-  T* h = ctx->d<T>("h", size_t(k) * n);
-  double* uw_d = ctx->d<double>("init.uw.d", size_t(m) * k);
-  double* uh_d = ctx->d<double>("init.uh.d", size_t(k) * n);
-  tm.span(kH2D, [&] {
-    RNMF_CUDA(cudaMemcpyAsync(uw_d, uw, sizeof(double) * size_t(m) * k, cudaMemcpyHostToDevice, ctx->stream));
-    RNMF_CUDA(cudaMemcpyAsync(uh_d, uh, sizeof(double) * size_t(k) * n, cudaMemcpyHostToDevice, ctx->stream));
-  });
-  tm.span(kInit, [&] {
-    tm.launches += launch_scale_cast<T>(uw_d, int64_t(m) * k, scale, w, ctx->stream);
-    tm.launches += launch_scale_cast<T>(uh_d, int64_t(k) * n, scale, h, ctx->stream);
-  });
+  if (!svd_init) {
+    double* uw_d = ctx->d<double>("init.uw.d", size_t(m) * k);
+    double* uh_d = ctx->d<double>("init.uh.d", size_t(k) * n);
+    tm.span(kH2D, [&] {
+      RNMF_CUDA(cudaMemcpyAsync(uw_d, uw, sizeof(double) * size_t(m) * k, cudaMemcpyHostToDevice, ctx->stream));
+      RNMF_CUDA(cudaMemcpyAsync(uh_d, uh, sizeof(double) * size_t(k) * n, cudaMemcpyHostToDevice, ctx->stream));
+    });
+    tm.span(kInit, [&] {
+      tm.launches += launch_scale_cast<T>(uw_d, int64_t(m) * k, scale, w, ctx->stream);
+      tm.launches += launch_scale_cast<T>(uh_d, int64_t(k) * n, scale, h, ctx->stream);
+    });
+  }
   double* wt = ctx->d<double>("wt", size_t(l) * k);
   const double x_norm = std::sqrt(eng.sumsq());
 
