@@ -208,6 +208,8 @@ struct SweepArgs {
   double* part;            // [2 * sweep_part_len(l,k) * grid]  (two alternating slots)
   double* fin;             // [2 * sweep_part_len(l,k)]
   long long* prof;         // optional: per-phase cycle counters of CTA 0 (kSweepProfSlots)
+  const int* order;        // Interleaved / Shuffled: component order, k per sweep of t_begin..t_end
+                           // (nullptr: Grouped)
 };
 bool sweep_prof_compiled();  // built with RNMF_SWEEP_PROF=1
 constexpr int kSweepProfSlots = 17;  // 16 buckets + barrier count

@@ -632,8 +632,9 @@ struct Sweeper {
     }
   }
 
-  // One column step of rhals_w_component (p/src/rhals.cpp:23-32); col_prepare(j) has run.
-  __device__ void w_column(int j) {
+  // One column step of rhals_w_component (p/src/rhals.cpp:23-32); col_prepare(j) has run.  With
+  // `chain`, the prologue of column j + 1 (grouped order) follows.
+  __device__ void w_column(int j, bool chain = true) {
     const double alpha = a.alpha_w, beta = a.beta_w;
     const double denom = fmax(Vm[j * k + j] + alpha, kDivisionFloor);
     prof_tick(kPfWStep);
@@ -847,7 +848,65 @@ struct Sweeper {
         wn[j] = v;
       }
     });
-    if (j + 1 < k) col_prepare(j + 1);
+    if (chain && j + 1 < k) col_prepare(j + 1);
+    __syncthreads();
+  }
+
+  // Interleaved / Shuffled orders (p/src/rhals.cpp:34-45,73-78): component j alone, with T(:,j) and
+  // V(:,j) recomputed from the current H (rhals_w_component_fresh), then row j of H against the
+  // new W~(:,j) (rhals_h_component_fresh -> clamped_row_update, p/src/hals.cpp:75-81).
+  __device__ void fresh_component(int j) {
+    // (a) t_j = B H(j,:)^T (l), v_j = H H(j,:)^T (k): partials over this CTA's columns, one barrier
+    const int L = l + k;
+    for (int e = tid; e < L; e += kSwThreads) {
+      const T* xa = e < l ? Bc + e * ncp : Hc + (e - l) * ncp;
+      const T* xb = Hc + j * ncp;
+      double s0 = 0.0, s1 = 0.0;
+      int64_t c = 0;
+      for (; c + 1 < NC; c += 2) {
+        s0 += double(xa[c]) * double(xb[c]);
+        s1 += double(xa[c + 1]) * double(xb[c + 1]);
+      }
+      if (c < NC) s0 += double(xa[c]) * double(xb[c]);
+      part_base()[int64_t(g) * L + e] = s0 + s1;
+    }
+    allreduce1(L, [&](int e, double v) {
+      if (e < l) {
+        Tm[e * kp + j] = v;
+      } else {
+        Vm[(e - l) * k + j] = v;
+        Vm[j * k + (e - l)] = v;
+      }
+    });
+    // P(:, j) = W~ v_j for the prologue
+    for (int i = tid; i < l; i += kSwThreads) {
+      double s = 0.0;
+      for (int c = 0; c < k; ++c) s += Wt[i * kp + c] * Vm[c * k + j];
+      Pm[i * kp + j] = s;
+    }
+    __syncthreads();
+    col_prepare(j);
+    __syncthreads();
+    w_column(j, false);
+    // (b) row j of H: s = W~^T W~(:,j) (replicated), then every owned column c (no reduction)
+    double* sv = colold;  // free after the column step (l >= k)
+    for (int i = tid; i < k; i += kSwThreads) {
+      double s = 0.0;
+      for (int a2 = 0; a2 < l; ++a2) s += Wt[a2 * kp + i] * Wt[a2 * kp + j];
+      sv[i] = s;
+    }
+    __syncthreads();
+    const double alpha = a.alpha_h, beta = a.beta_h;
+    const double denom = fmax(wn[j] + alpha, kDivisionFloor);
+    for (int64_t c = tid; c < NC; c += kSwThreads) {
+      double r = 0.0, sh = 0.0;
+      for (int i = 0; i < l; ++i) r += double(Bc[i * ncp + c]) * Wt[i * kp + j];
+      for (int i = 0; i < k; ++i) sh += sv[i] * double(Hc[i * ncp + c]);
+      const double hj = double(Hc[j * ncp + c]);
+      double num = r - sh - alpha * hj;
+      if (beta != 0.0) num -= beta;
+      Hc[j * ncp + c] = T(fmax(0.0, hj + num / denom));
+    }
     __syncthreads();
   }
 
@@ -1165,7 +1224,11 @@ struct Sweeper {
     const bool stationary = (a.flags & kRecord) && pg_rule && !(pgrad0 > 0.0);
     if (!stationary) {
       for (int64_t t = a.t_begin; t <= a.t_end; ++t) {
-        if (a.flags & kDoW) {
+        const bool fresh = a.order != nullptr;
+        if (fresh) {
+          const int* ord = a.order + (t - a.t_begin) * k;
+          for (int pos = 0; pos < k; ++pos) fresh_component(ord[pos]);
+        } else if (a.flags & kDoW) {
           compute_p();
           col_prepare(0);
           __syncthreads();
@@ -1173,7 +1236,9 @@ struct Sweeper {
         }
         if (a.flags & kDoH) {
           double objc = 0.0, pgh = 0.0;
-          h_phase(true, true, objc, pgh);
+          // fresh orders: H is already updated; evaluate with grad_H = -2 W~^T residc (the
+          // reference's scratch is invalid for them, p/src/rhals.cpp:79,155)
+          h_phase(!fresh, !fresh, objc, pgh);
           if (a.flags & kRecord) {
             const double pgw = pgrad_w();
             const double pgradc = pgw + pgh;

@@ -77,6 +77,7 @@ class Rng {
 };
 
 constexpr uint64_t kSketchStream = 3;  // p/include/rnmf/hals.hpp:107
+constexpr uint64_t kShuffleStream = 1;
 
 // ---- device / pinned buffers owned by a context ----------------------------------------------
 struct Buffer {
@@ -271,8 +272,8 @@ static void validate_options_after_data(int64_t m, int64_t n, const rnmf_solver_
 
 static void check_supported(const rnmf_solver_options& o) {
   if (o.init != RNMF_INIT_RANDOM && o.init != RNMF_INIT_SVD) throw ParameterError("unknown InitScheme");
-  if (o.order != RNMF_ORDER_GROUPED)
-    throw ParameterError("B200 path: only UpdateOrder::Grouped is implemented");
+  if (o.order != RNMF_ORDER_GROUPED && o.order != RNMF_ORDER_INTERLEAVED && o.order != RNMF_ORDER_SHUFFLED)
+    throw ParameterError("unknown UpdateOrder");
   if (o.reseed_dead) throw ParameterError("B200 path: reseed_dead is not implemented");
   if (o.math_mode != RNMF_MATH_EXACT && o.math_mode != RNMF_MATH_TF32X3 && o.math_mode != RNMF_MATH_TF32)
     throw ParameterError("math_mode must be RNMF_MATH_EXACT, RNMF_MATH_TF32X3 or RNMF_MATH_TF32");
@@ -727,6 +728,13 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   auto* hmres = ctx->h<double>("sw.mres.h", size_t(2 * max_evals));
   const bool objective_rule = o.stopping == RNMF_STOP_OBJECTIVE;
   const int64_t tfe = o.trace_full_every;
+  // Interleaved / Shuffled: the component order of every sweep of a chunk, drawn on the host from
+  // the reference shuffle stream (sweep_order, p/src/hals.cpp:83-94: Fisher-Yates with next_u64)
+  const bool fresh_order = o.order != RNMF_ORDER_GROUPED;
+  Rng shuffle_rng = Rng(o.seed).split(kShuffleStream);
+  const int64_t chunk_cap = objective_rule ? 1 : tfe;
+  int* hord = fresh_order ? ctx->h<int>("sw.order.h", size_t(chunk_cap * k)) : nullptr;
+  int* dord = fresh_order ? ctx->d<int>("sw.order", size_t(chunk_cap * k)) : nullptr;
   int64_t t_begin = 1;
   bool first = true;
   int64_t last = 0;
@@ -736,7 +744,21 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     a.flags = kRecord | kDoW | kDoH | (first ? (kEval0 | kInitWn | (io.init_wt ? kInitWt : 0)) : 0);
     a.t_begin = t_begin;
     a.t_end = t_end;
+    if (fresh_order) {
+      for (int64_t t = t_begin; t <= t_end; ++t) {
+        int* idx = hord + (t - t_begin) * k;
+        for (int j = 0; j < k; ++j) idx[j] = j;
+        if (o.order == RNMF_ORDER_SHUFFLED)
+          for (int i = k - 1; i > 0; --i) {
+            const int j = int(shuffle_rng.next_u64() % uint64_t(i + 1));
+            std::swap(idx[i], idx[j]);
+          }
+      }
+      RNMF_CUDA(cudaMemcpyAsync(dord, hord, sizeof(int) * size_t((t_end - t_begin + 1) * k), cudaMemcpyHostToDevice, st));
+      a.order = dord;
+    }
     tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
+    if (fresh_order) RNMF_CUDA(cudaStreamSynchronize(st));  // hord is rewritten for the next chunk
     RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
     if (prof) RNMF_CUDA(cudaMemcpyAsync(hprof, a.prof, kSweepProfSlots * sizeof(long long), cudaMemcpyDeviceToHost, st));
     RNMF_CUDA(cudaStreamSynchronize(st));
