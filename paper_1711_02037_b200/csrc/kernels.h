@@ -159,6 +159,8 @@ enum SweepFlags : int {
   kDoH = 32,      // H phase (+ evaluation) in each sweep
   kRecord = 64,   // write trace entries / stop checks
   kColOrdered = 128,  // column-step reduction through ordered fp64 partials (else fixed-point atomics)
+  kReseed = 256,      // reseed_dead: liveness stamps per sweep, stop at a dead component (host reseeds)
+  kEvalPrev = 512,    // evaluate + record sweep t_begin - 1 first (after a host-side reseed)
 };
 // Sync block of the sweep kernel (zeroed before every launch): the grid-barrier counter at byte 0,
 // then a 3-slot ring of 64-bit fixed-point accumulators for the column step.
@@ -197,7 +199,8 @@ struct SweepArgs {
   double* trace_objc;      // [max_iter + 1]
   double* trace_pgrad;     // [max_iter + 1]
   unsigned long long* trace_time;  // [max_iter + 1]
-  long long* status;       // [0] = last completed sweep, [1] = stopped flag
+  long long* status;       // [0] = last recorded sweep, [1] = stopped flag, [2] = sweep to reseed (0: none)
+  unsigned* alive;         // reseed_dead: [2k] last sweep in which W(:,j) / H(j,:) had a positive entry
   unsigned* barrier;       // sync block (kSweepSyncTotal; the first kSweepSyncBytes zeroed before launch)
   // row sharding: this process is `rank` of `world` GPUs; peer_sync[p] = GPU p's sync block mapped
   // into this process (peer_sync[rank] = barrier); xtotal = sum of the grids of all ranks.

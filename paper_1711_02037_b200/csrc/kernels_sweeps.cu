@@ -122,6 +122,8 @@ struct Sweeper {
   int slot = 0;
   unsigned long long* colacc;  // fixed-point column accumulators (3-slot ring)
   unsigned xepoch = 0;         // cross-GPU barriers passed (row-sharded runs)
+  unsigned cur_t = 0;          // sweep being computed (reseed_dead liveness stamps)
+  bool wpos = false;           // this thread lifted a positive W entry in the current column
   int xslot = 0;               // exchange-buffer slot of the next cross_allreduce
   unsigned cstep = 0;          // column steps done in this launch (ring position)
   double qrow[(QS && LREG > 0) ? LREG : 1];
@@ -653,6 +655,7 @@ struct Sweeper {
         double uu = (u[0] + u[1]) + (u[2] + u[3]);
         if (beta != 0.0) uu -= shift;
         wd = fmax(uu, 0.0);
+        wpos = wd > 0.0;
         wcold[tid] = wd;
         if constexpr (QS)
           WsT[int64_t(j) * RM + tid] = T(wd);
@@ -720,6 +723,7 @@ struct Sweeper {
           double uu2 = (u[0] + u[1]) + (u[2] + u[3]);
           if (beta != 0.0) uu2 -= shift;
           const double wd = fmax(uu2, 0.0);
+          wpos |= wd > 0.0;
           a.w[(r0 + r) * k + j] = T(wd);
 #pragma unroll
           for (int i = 0; i < LREG; ++i) acc[i] += (i < l ? double(qf[uu][i]) : (i == l ? wd : 0.0)) * wd;
@@ -770,6 +774,7 @@ struct Sweeper {
       double u = (u0 + u1) + (u2 + u3);
       if (beta != 0.0) u -= shift;
       const double wd = fmax(u, 0.0);
+      wpos |= wd > 0.0;
       wcold[r] = wd;
       if constexpr (QS)
         WsT[int64_t(j) * RM + r] = T(wd);
@@ -826,6 +831,11 @@ struct Sweeper {
     double cpart = 0.0;
     if (tid < L1)
       for (int w = 0; w < kSwWarps; ++w) cpart += red[w * kRedStride + tid];
+    if (a.flags & kReseed) {
+      // reseed_dead: stamp column j alive in this sweep if any of the CTA's rows lifted positive
+      if (__syncthreads_or(wpos) && tid == 0) atomicMax(a.alive + j, cur_t);
+      wpos = false;
+    }
     prof_tick(kPfRecomp);
     // W~(:,j) <- Q^T W(:,j) and P(i,:) += (W~_new(i,j) - W~_old(i,j)) V(j,:): thread i owns row i
     // of W~ and P, so the next column's prologue follows without a block barrier
@@ -898,6 +908,7 @@ struct Sweeper {
     __syncthreads();
     const double alpha = a.alpha_h, beta = a.beta_h;
     const double denom = fmax(wn[j] + alpha, kDivisionFloor);
+    bool hp = false;
     for (int64_t c = tid; c < NC; c += kSwThreads) {
       double r = 0.0, sh = 0.0;
       for (int i = 0; i < l; ++i) r += double(Bc[i * ncp + c]) * Wt[i * kp + j];
@@ -905,7 +916,12 @@ struct Sweeper {
       const double hj = double(Hc[j * ncp + c]);
       double num = r - sh - alpha * hj;
       if (beta != 0.0) num -= beta;
-      Hc[j * ncp + c] = T(fmax(0.0, hj + num / denom));
+      const T hv = T(fmax(0.0, hj + num / denom));
+      Hc[j * ncp + c] = hv;
+      hp |= hv > T(0);
+    }
+    if (a.flags & kReseed) {
+      if (__syncthreads_or(hp) && tid == 0) atomicMax(a.alive + k + j, cur_t);
     }
     __syncthreads();
   }
@@ -945,6 +961,7 @@ struct Sweeper {
     const int CPW = 32 / LPC;
     const int sub = lane / LPC, sl = lane % LPC;
     double objc_l = 0.0, pgh_l = 0.0;
+    unsigned long long hmask = 0ull;  // rows j of H with a positive entry here (reseed_dead)
     for (int64_t cb = int64_t(wid) * CPW; cb < NC; cb += int64_t(kSwWarps) * CPW) {
       const int64_t cl = cb + sub;
       const bool valid = cl < NC;
@@ -1051,7 +1068,11 @@ struct Sweeper {
         for (int t = 0; t < kMaxPerLane; ++t) {
           const int j = sl + LPC * t;
           if (j < k) {
-            if (update) Hc[j * ncp + cl] = T(h[t]);
+            if (update) {
+              const T hv = T(h[t]);
+              Hc[j * ncp + cl] = hv;
+              if (hv > T(0)) hmask |= 1ull << j;
+            }
             const double gval = grad_valid ? 2.0 * (acc[t] - r[t]) : -2.0 * gs[t];
             const double gp = h[t] > 0.0 ? gval : fmin(0.0, gval);
             pgh_l += gp * gp;
@@ -1060,6 +1081,17 @@ struct Sweeper {
       }
     }
     __syncthreads();
+    if (update && (a.flags & kReseed)) {
+      // reseed_dead: stamp the rows of H that keep a positive entry in this CTA's columns
+      __shared__ unsigned long long mask_s;
+      if (tid == 0) mask_s = 0ull;
+      __syncthreads();
+      if (hmask) atomicOr(&mask_s, hmask);
+      __syncthreads();
+      if (tid == 0)
+        for (int j = 0; j < k; ++j)
+          if ((mask_s >> j) & 1ull) atomicMax(a.alive + k + j, cur_t);
+    }
     prof_tick(kPfHCols);
     // CTA partial products: [T (l k) | V (k k) | E (l k) | objc | pgh]
     const int lk = l * k, kk = k * k, L = 2 * lk + kk + 2;
@@ -1220,10 +1252,21 @@ struct Sweeper {
     if (!(a.flags & kEval0)) pgrad0 = ld_cg(a.pgrad0);
     int64_t last = a.t_begin - 1;
     int stopped = 0;
+    int64_t reseed_at = 0;
     const bool pg_rule = a.stop_rule == 0;
     const bool stationary = (a.flags & kRecord) && pg_rule && !(pgrad0 > 0.0);
-    if (!stationary) {
+    if (a.flags & kEvalPrev) {
+      // after a host-side reseed of sweep t_begin - 1: its compressed evaluation with the new W, H
+      // (invalid scratch, p/src/rhals.cpp:182-188) and the stop test
+      double objc = 0.0, pgh = 0.0;
+      h_phase(false, false, objc, pgh);
+      const double pgradc = pgrad_w() + pgh;
+      record(a.t_begin - 1, objc, pgradc);
+      if (pg_rule && pgradc < a.tol * pgrad0) stopped = 1;
+    }
+    if (!stationary && !stopped) {
       for (int64_t t = a.t_begin; t <= a.t_end; ++t) {
+        cur_t = unsigned(t);
         const bool fresh = a.order != nullptr;
         if (fresh) {
           const int* ord = a.order + (t - a.t_begin) * k;
@@ -1237,8 +1280,18 @@ struct Sweeper {
         if (a.flags & kDoH) {
           double objc = 0.0, pgh = 0.0;
           // fresh orders: H is already updated; evaluate with grad_H = -2 W~^T residc (the
-          // reference's scratch is invalid for them, p/src/rhals.cpp:79,155)
-          h_phase(!fresh, !fresh, objc, pgh);
+          // reference's scratch is invalid for them, p/src/rhals.cpp:79,155; also with reseed_dead)
+          h_phase(!fresh, !fresh && !(a.flags & kReseed), objc, pgh);
+          if (a.flags & kReseed) {
+            // a component whose W column or H row has no positive entry left: hand the sweep to the
+            // host (reseed draws come from the reference stream), evaluated after the reseed
+            bool dead = false;
+            for (int j = 0; j < 2 * k; ++j) dead |= ld_cg(a.alive + j) != cur_t;
+            if (dead) {
+              reseed_at = t;
+              break;
+            }
+          }
           if (a.flags & kRecord) {
             const double pgw = pgrad_w();
             const double pgradc = pgw + pgh;
@@ -1260,6 +1313,7 @@ struct Sweeper {
       a.prof[kPfCount] = epoch;
     }
     store_back(last, stopped);
+    if (g == 0 && tid == 0) a.status[2] = reseed_at;
   }
 };
 

@@ -78,6 +78,7 @@ class Rng {
 
 constexpr uint64_t kSketchStream = 3;  // p/include/rnmf/hals.hpp:107
 constexpr uint64_t kShuffleStream = 1;
+constexpr uint64_t kReseedStream = 2;
 
 // ---- device / pinned buffers owned by a context ----------------------------------------------
 struct Buffer {
@@ -274,7 +275,7 @@ static void check_supported(const rnmf_solver_options& o) {
   if (o.init != RNMF_INIT_RANDOM && o.init != RNMF_INIT_SVD) throw ParameterError("unknown InitScheme");
   if (o.order != RNMF_ORDER_GROUPED && o.order != RNMF_ORDER_INTERLEAVED && o.order != RNMF_ORDER_SHUFFLED)
     throw ParameterError("unknown UpdateOrder");
-  if (o.reseed_dead) throw ParameterError("B200 path: reseed_dead is not implemented");
+
   if (o.math_mode != RNMF_MATH_EXACT && o.math_mode != RNMF_MATH_TF32X3 && o.math_mode != RNMF_MATH_TF32)
     throw ParameterError("math_mode must be RNMF_MATH_EXACT, RNMF_MATH_TF32X3 or RNMF_MATH_TF32");
 }
@@ -680,7 +681,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   a.trace_objc = ctx->d<double>("sw.tobjc", size_t(max_iter + 1));
   a.trace_pgrad = ctx->d<double>("sw.tpgrad", size_t(max_iter + 1));
   a.trace_time = ctx->d<unsigned long long>("sw.ttime", size_t(max_iter + 1));
-  a.status = ctx->d<long long>("sw.status", 2);
+  a.status = ctx->d<long long>("sw.status", 3);
   a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
@@ -724,7 +725,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   eng.metrics(k, io.w, io.h, mres);
   eval_iter.push_back(0);
 
-  auto* hstat = ctx->h<long long>("sw.status.h", 2);
+  auto* hstat = ctx->h<long long>("sw.status.h", 3);
   auto* hmres = ctx->h<double>("sw.mres.h", size_t(2 * max_evals));
   const bool objective_rule = o.stopping == RNMF_STOP_OBJECTIVE;
   const int64_t tfe = o.trace_full_every;
@@ -738,12 +739,16 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   int64_t t_begin = 1;
   bool first = true;
   int64_t last = 0;
+  // reseed_dead (p/src/rhals.cpp:182-186): liveness stamps per component, the reseed draws from
+  // the reference stream on the host when the kernel reports a dead component
+  Rng reseed_rng = Rng(o.seed).split(kReseedStream);
+  if (o.reseed_dead) {
+    a.alive = ctx->d<unsigned>("sw.alive", size_t(2) * k);
+    RNMF_CUDA(cudaMemsetAsync(a.alive, 0, sizeof(unsigned) * 2 * k, st));
+  }
   while (true) {
     // chunks end at the next full-metrics point (p/src/rhals.cpp:191-193)
     const int64_t t_end = std::min(max_iter, objective_rule ? t_begin : ceil_div(t_begin, tfe) * tfe);
-    a.flags = kRecord | kDoW | kDoH | (first ? (kEval0 | kInitWn | (io.init_wt ? kInitWt : 0)) : 0);
-    a.t_begin = t_begin;
-    a.t_end = t_end;
     if (fresh_order) {
       for (int64_t t = t_begin; t <= t_end; ++t) {
         int* idx = hord + (t - t_begin) * k;
@@ -755,15 +760,46 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
           }
       }
       RNMF_CUDA(cudaMemcpyAsync(dord, hord, sizeof(int) * size_t((t_end - t_begin + 1) * k), cudaMemcpyHostToDevice, st));
-      a.order = dord;
     }
-    tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
-    if (fresh_order) RNMF_CUDA(cudaStreamSynchronize(st));  // hord is rewritten for the next chunk
-    RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
-    if (prof) RNMF_CUDA(cudaMemcpyAsync(hprof, a.prof, kSweepProfSlots * sizeof(long long), cudaMemcpyDeviceToHost, st));
-    RNMF_CUDA(cudaStreamSynchronize(st));
-    if (prof)
-      for (int i = 0; i < kSweepProfSlots; ++i) prof_sum[size_t(i)] += hprof[i];
+    int extra = 0;
+    int64_t tb = t_begin;
+    while (true) {
+      a.flags = kRecord | kDoW | kDoH | (o.reseed_dead ? kReseed : 0) | extra |
+                (first ? (kEval0 | kInitWn | (io.init_wt ? kInitWt : 0)) : 0);
+      a.t_begin = tb;
+      a.t_end = t_end;
+      if (fresh_order) a.order = dord + (tb - t_begin) * k;
+      tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
+      RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 3 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      if (prof) RNMF_CUDA(cudaMemcpyAsync(hprof, a.prof, kSweepProfSlots * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      RNMF_CUDA(cudaStreamSynchronize(st));
+      if (prof)
+        for (int i = 0; i < kSweepProfSlots; ++i) prof_sum[size_t(i)] += hprof[i];
+      first = false;
+      if (hstat[2] == 0) break;
+      // reseed_dead_components (p/src/hals.cpp:96-105) after sweep t, in the reference's draw order
+      const int64_t t = hstat[2];
+      std::vector<unsigned> alive(static_cast<size_t>(2 * k));
+      RNMF_CUDA(cudaMemcpy(alive.data(), a.alive, sizeof(unsigned) * 2 * k, cudaMemcpyDeviceToHost));
+      T* hw = ctx->h<T>("reseed.w", size_t(io.m));
+      T* hh = ctx->h<T>("reseed.h", size_t(io.n));
+      for (int j = 0; j < k; ++j) {
+        if (alive[size_t(j)] != unsigned(t)) {
+          for (int64_t i = 0; i < io.m; ++i) hw[i] = T(reseed_rng.uniform() * 1e-4);
+          RNMF_CUDA(cudaMemcpy2DAsync(io.w + j, sizeof(T) * k, hw, sizeof(T), sizeof(T), size_t(io.m),
+                                      cudaMemcpyHostToDevice, st));
+          RNMF_CUDA(cudaStreamSynchronize(st));
+        }
+        if (alive[size_t(k + j)] != unsigned(t)) {
+          for (int64_t c = 0; c < io.n; ++c) hh[c] = T(reseed_rng.uniform() * 1e-4);
+          RNMF_CUDA(cudaMemcpyAsync(io.h + int64_t(j) * io.n, hh, sizeof(T) * size_t(io.n), cudaMemcpyHostToDevice, st));
+          RNMF_CUDA(cudaStreamSynchronize(st));
+        }
+      }
+      // W~ = Q^T W and the norms from the reseeded W, then the evaluation of sweep t
+      extra = kEvalPrev | kInitWt | kInitWn;
+      tb = t + 1;
+    }
     first = false;
     last = hstat[0];
     const bool stopped = hstat[1] != 0;
@@ -966,6 +1002,8 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   }
   T* om_dev = eng.upload_converted("omega", om, size_t(n) * l);
 
+  if (eng.sharded() && (o.reseed_dead || o.order != RNMF_ORDER_GROUPED))
+    throw ParameterError("B200 path: row-sharded fits support UpdateOrder::Grouped without reseed_dead");
   const bool svd_init = o.init == RNMF_INIT_SVD;
   if (svd_init && (w0 || h0)) throw ParameterError("init overrides require InitScheme::Random");
   if (svd_init && (m * n == 0 || k < 1)) throw ParameterError("InitScheme::Svd needs a non-empty X");
@@ -1049,7 +1087,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
     a.trace_objc = ctx->d<double>("sw.tobjc", 1);
     a.trace_pgrad = ctx->d<double>("sw.tpgrad", 1);
     a.trace_time = ctx->d<unsigned long long>("sw.ttime", 1);
-    a.status = ctx->d<long long>("sw.status", 2);
+    a.status = ctx->d<long long>("sw.status", 3);
     a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
     const int64_t plen = sweep_part_len(l, k);
     a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
@@ -1164,7 +1202,7 @@ static void stage_impl(rnmf_gpu_context* ctx, int location, const rnmf_problem_s
   a.trace_objc = ctx->d<double>("sw.tobjc", 2);
   a.trace_pgrad = ctx->d<double>("sw.tpgrad", 2);
   a.trace_time = ctx->d<unsigned long long>("sw.ttime", 2);
-  a.status = ctx->d<long long>("sw.status", 2);
+  a.status = ctx->d<long long>("sw.status", 3);
   a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
   const int64_t plen = sweep_part_len(l, k);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
