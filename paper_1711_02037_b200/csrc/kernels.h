@@ -69,10 +69,10 @@ template <typename T>
 int launch_metrics_fused(const T* x, int64_t m, int64_t n, int64_t ldx, const T* w, const T* h, int k,
                          const double* hht, T* hpad, T* wtx_part, double* part_obj, double* part_pgw, int sm_count,
                          cudaStream_t stream);
-// 2-D row-major tensor map (rows x cols, pitch in elements), box = box_rows x box_cols, no swizzle,
-// zero fill out of bounds (kernels_tc.cu)
+// 2-D row-major tensor map (rows x cols, pitch in elements), box = box_rows x box_cols, zero fill
+// out of bounds; swizzle128: SWIZZLE_128B (box rows of 128 bytes, 16-byte chunk index XOR row % 8)
 CUtensorMap make_tma_2d(const void* base, int elem_bytes, int64_t rows, int64_t cols, int64_t pitch, int box_cols,
-                        int box_rows);
+                        int box_rows, bool swizzle128 = false);
 
 // ---- small dense helpers (kernels_xgemm.cu) ---------------------------------------------------
 // G (c x c, fp64) = A^T A for A (rows x c) row-major.  part: gram_parts(rows)*c*c doubles.

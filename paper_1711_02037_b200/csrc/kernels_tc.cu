@@ -485,7 +485,7 @@ void tc_xtw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const floa
 }  // namespace
 
 CUtensorMap make_tma_2d(const void* base, int elem_bytes, int64_t rows, int64_t cols, int64_t pitch, int box_cols,
-                        int box_rows) {
+                        int box_rows, bool swizzle128) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
   const cuuint64_t strides[1] = {cuuint64_t(pitch) * cuuint64_t(elem_bytes)};
@@ -493,7 +493,8 @@ CUtensorMap make_tma_2d(const void* base, int elem_bytes, int64_t rows, int64_t 
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                  2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return m;
