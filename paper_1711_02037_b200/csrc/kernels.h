@@ -23,6 +23,12 @@ int launch_scan(const T* x, int64_t count, unsigned long long* bad, double* part
 // Y (m x c) = X (m x n) * S (n x c).  All row-major, leading dims = column counts.
 template <typename T>
 int launch_xw(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* y, cudaStream_t stream);
+// The same through TMA-fed, register-blocked FMA tiles (kernels_xw.cu); X rows 16-byte aligned.
+// spad: scratch of xw_tma_spad_len(n, c) elements (S zero-padded to the kernel's column count).
+int64_t xw_tma_spad_len(int64_t n, int c);
+template <typename T>
+int launch_xw_tma(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* y, T* spad, int sm_count,
+                  cudaStream_t stream);
 
 // Fused full-space metrics pass 1 over X: with S = H^T (n x k) and W (m x k):
 //   part_obj[b]  = partial sum of (X - W H)^2 over CTA b's rows

@@ -474,7 +474,12 @@ class Engine {
             return;
           }
         }
-        tm_.launches += launch_xw<T>(x, m, n, ldx, s, l, out, st_);
+        if (!std::getenv("RNMF_XW_LEGACY")) {  // testing knob: the previous register-staged kernel
+          T* spad = ctx_->d<T>("rqb.spad", size_t(xw_tma_spad_len(n, l)));
+          tm_.launches += launch_xw_tma<T>(x, m, n, ldx, s, l, out, spad, ctx_->sm_count, st_);
+        } else {
+          tm_.launches += launch_xw<T>(x, m, n, ldx, s, l, out, st_);
+        }
       });
       sketch_bytes_ += xbytes;
       ctx_->last.xw_bytes += xbytes;
