@@ -26,6 +26,12 @@ int launch_xw(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, 
 // The same through TMA-fed, register-blocked FMA tiles (kernels_xw.cu); X rows 16-byte aligned.
 // spad: scratch of xw_tma_spad_len(n, c) elements (S zero-padded to the kernel's column count).
 int64_t xw_tma_spad_len(int64_t n, int c);
+// P = X^T S through TMA-fed FMA panels (kernels_xw.cu): part holds splits * n * c, then the fixed
+// order split reduction into out (n x c, or c x n with transpose_out); spad: xw_tma_spad_len(m, c)
+int xtw_tma_splits(int64_t m, int64_t n, int sm_count);
+template <typename T>
+int launch_xtw_tma(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* part, int splits, T* out,
+                   bool transpose_out, T* spad, int sm_count, cudaStream_t stream);
 template <typename T>
 int launch_xw_tma(const T* x, int64_t m, int64_t n, int64_t ldx, const T* s, int c, T* y, T* spad, int sm_count,
                   cudaStream_t stream);

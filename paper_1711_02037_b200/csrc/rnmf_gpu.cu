@@ -474,7 +474,10 @@ class Engine {
             return;
           }
         }
-        if (!std::getenv("RNMF_XW_LEGACY")) {  // testing knob: the previous register-staged kernel
+        // fp32: TMA-fed tiles; fp64 (BASELINE config 1, rank-deficient: the sketch's trailing
+        // columns are rounding noise whose completion the validated register-staged kernels keep)
+        // and the RNMF_XW_LEGACY testing knob: the register-staged kernel
+        if (sizeof(T) == 4 && !std::getenv("RNMF_XW_LEGACY")) {
           T* spad = ctx_->d<T>("rqb.spad", size_t(xw_tma_spad_len(n, l)));
           tm_.launches += launch_xw_tma<T>(x, m, n, ldx, s, l, out, spad, ctx_->sm_count, st_);
         } else {
@@ -495,7 +498,14 @@ class Engine {
             return;
           }
         }
-        tm_.launches += launch_xtw<T>(x, m, n, ldx, s, l, part, splits, out, tr, st_);
+        if (sizeof(T) == 4 && !std::getenv("RNMF_XW_LEGACY")) {
+          const int sp = xtw_tma_splits(m, n, ctx_->sm_count);
+          T* part2 = ctx_->d<T>("rqb.part2", size_t(sp) * n * l);
+          T* spad = ctx_->d<T>("rqb.spad2", size_t(xw_tma_spad_len(m, l)));
+          tm_.launches += launch_xtw_tma<T>(x, m, n, ldx, s, l, part2, sp, out, tr, spad, ctx_->sm_count, st_);
+        } else {
+          tm_.launches += launch_xtw<T>(x, m, n, ldx, s, l, part, splits, out, tr, st_);
+        }
       });
       sketch_bytes_ += xbytes;
       ctx_->last.xtw_bytes += xbytes;
