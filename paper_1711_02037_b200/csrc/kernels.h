@@ -243,6 +243,7 @@ struct SweepPlan {
   int64_t rows_per_cta = 0;
   int64_t cols_per_cta = 0;
   int lreg = 0;  // > 0: Q rows register-resident (rows_per_cta <= 256, l + 1 <= lreg <= 64)
+  int qring = 0;  // > 0: streamed slabs through a shared-memory bulk-copy ring of that many stages
 };
 template <typename T>
 SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem);

@@ -25,6 +25,7 @@
 // partials another CTA is still reading.
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -57,10 +58,13 @@ struct SmemLayout {
   size_t wt, tm, em, vm, sm, wn, pm, colold, colnew, invd, red, scal, doubles_end;
   // T region (offsets in bytes from the start)
   size_t qs, wst, wcold, bc, hc, rc, total;
+  // streamed Q slabs through a 2-stage bulk-copy ring (0: not used): stage = kSwThreads rows
+  size_t qring, qring_stage, qbars, qring_n;
 };
 
+constexpr int kQRingMax = 6;  // bulk-copy ring stages (fewer when shared memory is short)
 template <typename T>
-SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
+SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring = 0) {
   SmemLayout L{};
   size_t d = 0;
   auto take = [&](size_t count) {  // 16-byte aligned (double2 loads)
@@ -76,7 +80,7 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
   L.wn = take(size_t(k));
   L.pm = take(size_t(l) * (k + 1));
   L.colold = take(size_t(l));
-  L.colnew = take(size_t(l));
+  L.colnew = take(size_t(l) > 64 ? size_t(l) : 64);  // zero past l: branch-free padded dot products
   L.invd = take(size_t(k));
   L.red = take(kRedLen + 2 * kSwWarps);
   L.scal = take(16);
@@ -94,11 +98,20 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs) {
     return off;
   };
   L.qs = qs ? takeD(size_t(RM) * (l + 1)) : 0;
-  L.wcold = takeD(size_t(RM));
+  L.wcold = ring ? 0 : takeD(size_t(RM));  // the ring path keeps the lifted column in registers
   L.wst = qs ? takeT(size_t(k) * RM) : 0;
   L.bc = takeT(size_t(l) * ncp);
   L.hc = takeT(size_t(k) * ncp);
   L.rc = takeT(size_t(l) * ncp);
+  if (ring) {
+    b = (b + 127) / 128 * 128;
+    L.qring_stage = size_t(kSwThreads) * l * sizeof(T);
+    L.qring = b;
+    L.qring_n = size_t(ring);
+    b += size_t(ring) * L.qring_stage;
+    L.qbars = b;
+    b += 8 * size_t(ring);
+  }
   L.total = b;
   return L;
 }
@@ -121,6 +134,13 @@ struct Sweeper {
   unsigned epoch = 0;
   int slot = 0;
   unsigned long long* colacc;  // fixed-point column accumulators (3-slot ring)
+  // streamed Q slab ring (L.qring): chunks of kSwThreads rows, 2 stages, prefetch runs ahead across
+  // columns (Q is constant, so the next pass's first chunks load while the column reduction waits)
+  const T* qring = nullptr;
+  uint64_t* qbars = nullptr;
+  size_t qstage_elems = 0;
+  int qst = 0;  // stages
+  int64_t qnch = 0, qissued = 0, qused = 0;
   unsigned xepoch = 0;         // cross-GPU barriers passed (row-sharded runs)
   unsigned cur_t = 0;          // sweep being computed (reseed_dead liveness stamps)
   bool wpos = false;           // this thread lifted a positive W entry in the current column
@@ -179,6 +199,17 @@ struct Sweeper {
     Hc = reinterpret_cast<T*>(smem + L.hc);
     Rc = reinterpret_cast<T*>(smem + L.rc);
     colacc = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(a.barrier) + 128);
+    if (L.qring) {
+      qring = reinterpret_cast<const T*>(smem + L.qring);
+      qbars = reinterpret_cast<uint64_t*>(smem + L.qbars);
+      qstage_elems = size_t(kSwThreads) * l;
+      qnch = (R + kSwThreads - 1) / kSwThreads;
+      qst = int(L.qring_n);
+      if (tid == 0) {
+        for (int s2 = 0; s2 < qst; ++s2) tc::mbar_init(&qbars[s2], 1);
+        tc::fence_mbar_init();
+      }
+    }
     part_slot_len = sweep_part_len(l, k) * G;
     fin_slot_len = sweep_part_len(l, k);
     prof_on = kSweepProf && a.prof != nullptr && g == 0 && tid == 0;
@@ -253,6 +284,20 @@ struct Sweeper {
     }
     __syncthreads();
   }
+  // thread 0: bulk-copy chunk c (global chunk counter; chunk c % qnch of the slab) into stage c & 1
+  __device__ void qring_issue(int64_t c) {
+    const int st = int(c % qst);
+    const int64_t cc = c % qnch, rows = min(int64_t(kSwThreads), R - cc * kSwThreads);
+    const uint32_t bytes = uint32_t(rows * l * int64_t(sizeof(T)));
+    tc::mbar_arrive_expect_tx(&qbars[st], bytes);
+    tc::bulk_load(const_cast<T*>(qring) + st * qstage_elems, a.q + (r0 + cc * kSwThreads) * l, bytes, &qbars[st]);
+  }
+  // before the CTA exits: every issued chunk has landed (no bulk copy may target a dead CTA)
+  __device__ void qring_drain() {
+    if (!qring) return;
+    for (int64_t c = qused; c < qissued; ++c) tc::mbar_wait(&qbars[c % qst], uint32_t((c / qst) & 1));
+  }
+
   // All-reduce over GPUs of L values that are already identical in every CTA of a GPU (the result
   // of a GPU-local reduction): CTA 0 stores its GPU's values into slot [xslot][rank] of every
   // GPU's exchange buffer, one cross barrier, then every CTA sums the world contributions in rank
@@ -440,6 +485,7 @@ struct Sweeper {
 
   // ---------------------------------------------------------------------------------------------
   __device__ void load_resident() {
+    for (int i = tid; i < 64; i += kSwThreads) colnew[i] = 0.0;  // the padded tail stays zero
     if constexpr (QS) {
       for (int64_t e = tid; e < R * l; e += kSwThreads) {
         const int64_t r = e / l;
@@ -700,9 +746,63 @@ struct Sweeper {
       }
     } else if constexpr (LREG > 0) {
       // streamed rows (Q slab not resident): one pass, row in registers, fp64 accumulators
-      double acc[LREG];
+      double acc[LREG], accn = 0.0;
 #pragma unroll
       for (int i = 0; i < LREG; ++i) acc[i] = 0.0;
+      if (qring) {
+        // the slab arrives chunk by chunk through the bulk-copy ring; thread t takes row t of a chunk
+        if (qissued == 0) {
+          if (tid == 0)
+            for (int c2 = 0; c2 < qst; ++c2) qring_issue(c2);
+          qissued = qst;
+        }
+        for (int64_t cc = 0; cc < qnch; ++cc) {
+          const int64_t c = qused;
+          tc::mbar_wait(&qbars[c % qst], uint32_t((c / qst) & 1));
+          const int64_t r = cc * kSwThreads + tid;
+          if (r < R) {
+            const T* qr = qring + (c % qst) * qstage_elems + int64_t(tid) * l;
+            T qf[LREG];
+            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+              for (int i4 = 0; i4 < LREG / 4; ++i4) {
+                if (i4 * 4 < l) {
+                  const float4 v4 = reinterpret_cast<const float4*>(qr)[i4];
+                  qf[4 * i4] = v4.x, qf[4 * i4 + 1] = v4.y, qf[4 * i4 + 2] = v4.z, qf[4 * i4 + 3] = v4.w;
+                } else {
+                  qf[4 * i4] = qf[4 * i4 + 1] = qf[4 * i4 + 2] = qf[4 * i4 + 3] = T(0);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int i2 = 0; i2 < LREG / 2; ++i2) {
+                if (i2 * 2 < l) {
+                  const double2 v2 = reinterpret_cast<const double2*>(qr)[i2];
+                  qf[2 * i2] = v2.x, qf[2 * i2 + 1] = v2.y;
+                } else {
+                  qf[2 * i2] = qf[2 * i2 + 1] = T(0);
+                }
+              }
+            }
+            double u[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int i = 0; i < LREG; ++i)
+              u[i & 3] += double(qf[i]) * colnew[i];  // qf, colnew zero past l
+            double uu2 = (u[0] + u[1]) + (u[2] + u[3]);
+            if (beta != 0.0) uu2 -= shift;
+            const double wd = fmax(uu2, 0.0);
+            wpos |= wd > 0.0;
+            a.w[(r0 + r) * k + j] = T(wd);
+#pragma unroll
+            for (int i = 0; i < LREG; ++i) acc[i] += double(qf[i]) * wd;
+            accn += wd * wd;
+          }
+          __syncthreads();  // stage c % qst consumed by every thread
+          qused = c + 1;
+          if (tid == 0) qring_issue(c + qst);
+          qissued = c + 1 + qst;
+        }
+      } else {
       // UNR rows per thread per iteration, all their loads issued before any is used
       constexpr int UNR = (sizeof(T) == 4 && LREG <= 32) ? 4 : 1;
       for (int64_t rb = tid; rb < R; rb += int64_t(kSwThreads) * UNR) {
@@ -719,15 +819,17 @@ struct Sweeper {
           double u[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int i = 0; i < LREG; ++i)
-            if (i < l) u[i & 3] += double(qf[uu][i]) * colnew[i];
+            u[i & 3] += double(qf[uu][i]) * colnew[i];
           double uu2 = (u[0] + u[1]) + (u[2] + u[3]);
           if (beta != 0.0) uu2 -= shift;
           const double wd = fmax(uu2, 0.0);
           wpos |= wd > 0.0;
           a.w[(r0 + r) * k + j] = T(wd);
 #pragma unroll
-          for (int i = 0; i < LREG; ++i) acc[i] += (i < l ? double(qf[uu][i]) : (i == l ? wd : 0.0)) * wd;
+          for (int i = 0; i < LREG; ++i) acc[i] += double(qf[uu][i]) * wd;
+          accn += wd * wd;
         }
+      }
       }
       prof_tick(kPfLift);
 #pragma unroll
@@ -739,8 +841,9 @@ struct Sweeper {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int ia = chunk * 32 + e, ib = ia + 16;
-              const double va = ia < LREG ? acc[ia < LREG ? ia : 0] : 0.0;
-              const double vb = ib < LREG ? acc[ib < LREG ? ib : 0] : 0.0;
+              // entry l (the squared norm) lives in accn; acc[l] is zero (qf is zero past l)
+              const double va = (ia < LREG ? acc[ia < LREG ? ia : 0] : 0.0) + (ia == l ? accn : 0.0);
+              const double vb = (ib < LREG ? acc[ib < LREG ? ib : 0] : 0.0) + (ib == l ? accn : 0.0);
               const double send = hi ? va : vb;
               const double mine = hi ? vb : va;
               v[e] = mine + __shfl_xor_sync(0xffffffffu, send, 16);
@@ -1312,6 +1415,7 @@ struct Sweeper {
       for (int b = 0; b < kPfCount; ++b) a.prof[b] = prof_acc[b];
       a.prof[kPfCount] = epoch;
     }
+    qring_drain();
     store_back(last, stopped);
     if (g == 0 && tid == 0) a.status[2] = reseed_at;
   }
@@ -1343,8 +1447,18 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
       p.grid = G;
       if (p.q_in_smem && p.rows_per_cta <= kSwThreads && l + 1 <= 64 && !std::getenv("RNMF_NO_QREG"))
         p.lreg = (l + 1 <= 32) ? 32 : (l + 1 <= 48) ? 48 : 64;
-      if (!p.q_in_smem && !std::getenv("RNMF_NO_QSTREAM") && (l + 1 <= 32 || (sizeof(T) == 4 && l + 1 <= 64)))
+      if (!p.q_in_smem && !std::getenv("RNMF_NO_QSTREAM") && (l + 1 <= 32 || (sizeof(T) == 4 && l + 1 <= 64))) {
         p.lreg = (l + 1 <= 32) ? 32 : 64;
+        // bulk-copy ring for the streamed slab: 16-byte row pitch, the ring must fit as well
+        for (int st = kQRingMax; st >= 2 && !p.qring; --st) {
+          const SmemLayout LR = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, false, st);
+          if ((int64_t(l) * int64_t(sizeof(T))) % 16 == 0 && LR.total <= size_t(max_smem) &&
+              !std::getenv("RNMF_NO_QRING")) {
+            p.qring = st;
+            p.smem = LR.total;
+          }
+        }
+      }
       return p;
     }
   }
@@ -1354,7 +1468,8 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
 template <typename T>
 int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream) {
   if (plan.grid <= 0) throw CudaError("sweeps: problem does not fit the persistent kernel");
-  const SmemLayout L = make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem);
+  const SmemLayout L =
+      make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem, plan.qring);
   RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, kSweepSyncBytes, stream));
   if (args.l + 1 > kColAccMax) throw CudaError("sweeps: sketch width above the column-reduction capacity");
   SweepArgs<T> a = args;
