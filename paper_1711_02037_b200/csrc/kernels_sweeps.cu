@@ -55,7 +55,7 @@ enum {
 
 struct SmemLayout {
   // fp64 region
-  size_t wt, tm, em, vm, sm, wn, pm, colold, colnew, invd, red, scal, doubles_end;
+  size_t wt, tm, em, vm, sm, wn, pm, colold, colnew, invd, rdw, red, scal, doubles_end;
   // T region (offsets in bytes from the start)
   size_t qs, wst, wcold, bc, hc, rc, total;
   // streamed Q slabs through a 2-stage bulk-copy ring (0: not used): stage = kSwThreads rows
@@ -82,6 +82,7 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring 
   L.colold = take(size_t(l));
   L.colnew = take(size_t(l) > 64 ? size_t(l) : 64);  // zero past l: branch-free padded dot products
   L.invd = take(size_t(k));
+  L.rdw = take(size_t(k));
   L.red = take(kRedLen + 2 * kSwWarps);
   L.scal = take(16);
   L.doubles_end = d * sizeof(double);
@@ -128,7 +129,7 @@ struct Sweeper {
   int G, g, tid, lane, wid, l, k;
   int64_t r0, R, c0, NC, RM;
   int ncp, lq, kp;  // kp = k + 1: odd fp64 row stride of the l x k arrays (bank-conflict free columns)
-  double *Wt, *Tm, *Em, *Vm, *Sm, *wn, *Pm, *colold, *colnew, *invd, *red, *scal;
+  double *Wt, *Tm, *Em, *Vm, *Sm, *wn, *Pm, *colold, *colnew, *invd, *rdw, *red, *scal;
   double *Qs, *wcold;
   T *WsT, *Bc, *Hc, *Rc;
   unsigned epoch = 0;
@@ -190,6 +191,7 @@ struct Sweeper {
     colold = D + L.colold;
     colnew = D + L.colnew;
     invd = D + L.invd;
+    rdw = D + L.rdw;
     red = D + L.red;
     scal = D + L.scal;
     Qs = QS ? reinterpret_cast<double*>(smem + L.qs) : nullptr;
@@ -657,6 +659,8 @@ struct Sweeper {
       if (t < k) s0 += wi[t] * Vm[t * k + c];
       Pm[i * kp + c] = s0 + s1;
     }
+    // reciprocal step denominators of the sweep's columns (off the column chain)
+    for (int j = tid; j < k; j += kSwThreads) rdw[j] = 1.0 / fmax(Vm[j * k + j] + a.alpha_w, kDivisionFloor);
     __syncthreads();
   }
 
@@ -664,14 +668,15 @@ struct Sweeper {
   // colnew(i) = W~(i,j) + (T(i,j) - P(i,j) - alpha W~(i,j)) / denom_j, plus the per-warp
   // ||colnew||^2 that bounds the fixed-point column reduction (fixed order: identical on every
   // CTA).  Caller synchronises before colnew is read by other threads.
-  __device__ void col_prepare(int j) {
+  __device__ void col_prepare(int j, bool fresh = false) {
     const double alpha = a.alpha_w;
-    const double denom = fmax(Vm[j * k + j] + alpha, kDivisionFloor);
+    // grouped sweeps: 1 / denom precomputed in compute_p (the fresh orders recompute V(j,j))
+    const double rden = fresh ? 1.0 / fmax(Vm[j * k + j] + alpha, kDivisionFloor) : rdw[j];
     if (wid * 32 < l) {
       double nw = 0.0;
       if (tid < l) {
         const double cur = Wt[tid * kp + j];
-        nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) / denom;
+        nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) * rden;
         colold[tid] = cur;
         colnew[tid] = nw;
       }
@@ -998,7 +1003,7 @@ struct Sweeper {
       Pm[i * kp + j] = s;
     }
     __syncthreads();
-    col_prepare(j);
+    col_prepare(j, true);
     __syncthreads();
     w_column(j, false);
     // (b) row j of H: s = W~^T W~(:,j) (replicated), then every owned column c (no reduction)
