@@ -105,6 +105,9 @@ template <typename T>
 int launch_widen(const T* in, int64_t count, double* out, cudaStream_t stream);
 // sum of `count` doubles in fixed order -> out[0]
 int launch_sum_parts(const double* part, int count, double* out, cudaStream_t stream);
+// res[0] = sum of pobj, res[1] = sum of ppgw + sum of ppgh (one launch)
+int launch_metrics_finalize(const double* pobj, int nobj, const double* ppgw, int npgw, const double* ppgh, int npgh,
+                            double* res, cudaStream_t stream);
 // out[e] = sum_p part[p * len + e], fixed order
 int launch_reduce_parts(const double* part, int nparts, int len, double* out, cudaStream_t stream);
 // writes %globaltimer to *out

@@ -598,6 +598,25 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int count, dou
   if (threadIdx.x == 0) out[0] = v;
 }
 
+// res[0] = sum(pobj), res[1] = sum(ppgw) + sum(ppgh): the three partial sums of the metrics in one
+// warp each (fixed order), one launch
+__global__ void metrics_finalize_kernel(const double* __restrict__ pobj, int nobj, const double* __restrict__ ppgw,
+                                        int npgw, const double* __restrict__ ppgh, int npgh, double* res) {
+  __shared__ double v3[3];
+  const int w = threadIdx.x / 32;
+  const double* p = w == 0 ? pobj : w == 1 ? ppgw : ppgh;
+  const int cnt = w == 0 ? nobj : w == 1 ? npgw : npgh;
+  double v = 0.0;
+  for (int i = lane_id(); i < cnt; i += 32) v += p[i];
+  v = warp_allreduce_sum(v);
+  if (lane_id() == 0) v3[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    res[0] = v3[0];
+    res[1] = v3[1] + v3[2];
+  }
+}
+
 __global__ void timestamp_kernel(unsigned long long* out) { *out = globaltimer_ns(); }
 
 template <typename F>
@@ -798,6 +817,13 @@ int launch_widen(const T* in, int64_t count, double* out, cudaStream_t stream) {
 
 int launch_reduce_parts(const double* part, int nparts, int len, double* out, cudaStream_t stream) {
   reduce_parts_kernel<<<unsigned(ceil_div(len, 64)), 256, 0, stream>>>(part, nparts, len, out);
+  RNMF_CUDA_LAUNCH();
+  return 1;
+}
+
+int launch_metrics_finalize(const double* pobj, int nobj, const double* ppgw, int npgw, const double* ppgh, int npgh,
+                            double* res, cudaStream_t stream) {
+  metrics_finalize_kernel<<<1, 96, 0, stream>>>(pobj, nobj, ppgw, npgw, ppgh, npgh, res);
   RNMF_CUDA_LAUNCH();
   return 1;
 }

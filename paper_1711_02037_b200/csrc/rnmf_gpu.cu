@@ -554,7 +554,8 @@ class Engine {
 
   // Full-space metrics (p/src/rhals.cpp:140-148) of the device factors w (m x k), h (k x n):
   // writes [objective, pgrad_full] into res (device).
-  void metrics(int k, const T* w, const T* h, double* res) {
+  // hht_in: H H^T (k x k, fp64) when the caller has it (the sweep kernel's V after every launch)
+  void metrics(int k, const T* w, const T* h, double* res, const double* hht_in = nullptr) {
     const T* x = x_;
     const int64_t m = m_, n = n_, ldx = ldx_;
     T* ht = ctx_->d<T>("met.ht", size_t(n) * k);
@@ -578,7 +579,10 @@ class Engine {
     x_passes_ = 2;
     if (sharded() && !one_pass) throw ParameterError("B200 path: row-sharded metrics need the one-pass kernel (k <= 64)");
     tm_.span(kMetrics, [&] {
-      tm_.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st_);
+      if (hht_in)
+        hht = const_cast<double*>(hht_in);
+      else
+        tm_.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st_);
       tm_.launches += launch_gram_rows<T>(w, m, k, gpart2, wtw, st_);
       allreduce(wtw, size_t(k) * k);  // W^T W over all rows (H H^T is replicated)
       int b1 = 0, b2 = 0;
@@ -614,16 +618,18 @@ class Engine {
         tm_.launches += launch_xw_metrics<T>(x, m, n, ldx, ht, w, k, hht, pobj, ppgw, &b1, st_);
         tm_.launches += launch_xtw_metrics<T>(x, m, n, ldx, w, k, h, wtw, part, splits, ppgh, &b2, st_);
       }
-      tm_.launches += launch_sum_parts(pobj, b1, res, st_);
-      tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
-      if (sharded()) {
+      if (!sharded()) {
+        tm_.launches += launch_metrics_finalize(pobj, b1, ppgw, b1, ppgh, b2, res, st_);
+      } else {
+        tm_.launches += launch_sum_parts(pobj, b1, res, st_);
+        tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
         // objective and the grad_W term are sums over rows: add the GPUs' values (grad_H is replicated)
         allreduce(res, 1);
         allreduce(tmp, 1);
+        tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
+        // res[1] = pgw + pgh, done on device by a 2-element sum
+        tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
       }
-      tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
-      // res[1] = pgw + pgh, done on device by a 2-element sum
-      tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
     });
     metrics_bytes_ += double(x_passes_) * double(m) * double(n) * sizeof(T);
     metrics_passes_ += x_passes_;
@@ -819,7 +825,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     last = hstat[0];
     const bool stopped = hstat[1] != 0;
     if (last >= t_begin) {
-      eng.metrics(k, io.w, io.h, mres + 2 * eval_iter.size());
+      eng.metrics(k, io.w, io.h, mres + 2 * eval_iter.size(), a.vm);  // V = H H^T of the final H
       eval_iter.push_back(last);
     }
     bool stop = stopped;
