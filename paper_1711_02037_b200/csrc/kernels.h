@@ -115,6 +115,7 @@ int launch_timestamp(unsigned long long* out, cudaStream_t stream);
 
 // ---- tcgen05 tensor-core X-streaming GEMMs (kernels_tc.cu, fp32 X only) ------------------------
 int tc_npad(int c);               // UMMA N for c output columns (multiple of 16)
+void tc_set_chunk(int stages);    // K stages per TMEM accumulation chunk (tests / probes)
 int64_t tc_st_pitch(int64_t n);   // pitch of the S^T operand
 // S (n x c) -> S^T split into tf32 hi and fp32 lo parts (tc_npad(c) x tc_st_pitch(n) each)
 int launch_tc_prep_st(const float* s, int64_t n, int c, float* st_hi, float* st_lo, cudaStream_t stream);

@@ -2,14 +2,23 @@
 //
 //   tc_xw : Y (m x c) = X (m x n) * S (n x c)        sketch Y = X Omega, Y = X Z (p/src/sketch.cpp:60,64)
 //
-// Structure (one persistent CTA per SM, 8 warps, warp-specialised):
-//   warp 0      TMA producer: X tile (128 rows x 32 cols fp32 = 16 KB, SWIZZLE_128B) and the
-//               matching 32-column slab of S^T (N rows x 128 B) into a kStages-deep ring.
-//   warp 1      TMEM allocator + single-thread UMMA issue: per stage 4 x tcgen05.mma kind::tf32
-//               (M=128, N=NPAD, K=8), accumulator in TMEM, double-buffered across row tiles.
-//   warps 2-3   (3xTF32 only) split the X tile in place into tf32 hi and a separate lo tile,
-//               so D = X_hi S_hi + X_hi S_lo + X_lo S_hi keeps fp32 accuracy.
-//   warps 4-7   epilogue: tcgen05.ld of the 128 x NPAD accumulator, rows written to Y.
+//   tc_xtw: part (n x c) = X^T (n x m) * S (m x c)   X^T Q, B^T = X^T Q    (p/src/sketch.cpp:63,69)
+//
+// Structure (one persistent CTA per SM, warp-specialised):
+//   warp 0       TMA producer: X tile (16 KB, 128 B swizzle) and the matching S^T slab(s) into a
+//                ring of kStages stages.
+//   warp 1       TMEM allocator + single-thread UMMA issue (tcgen05.mma kind::tf32, M = 128).
+//   warps 2-3, 8-11 (3xTF32 only) write lo = rna_tf32(X - trunc_tf32(X)) into a 3-slot lo ring;
+//                the raw X tile is the hi operand (kind::tf32 truncates), so per K step
+//                  D[0:2N)  = X_hi [S_hi; S_lo]^T   (one UMMA, N = 2 NPAD)
+//                  D[2N:3N) = X_lo S_hi^T
+//                and the big term never shares an accumulator with the small ones.
+//   warps 4-7    epilogue: every chunk of p.chunk stages lands in a fresh TMEM buffer that the
+//                epilogue adds into fp32 registers (round-to-nearest), which bounds the tensor
+//                core's truncating accumulation to p.chunk * 32 terms.  Measured on B200
+//                (tools/sketch_acc.cu): 3xTF32 with 64-term chunks is as accurate as the FFMA
+//                kernels (rms error 7e-7 vs 8e-7 of the result), where whole-K accumulation was
+//                2e-5 - 1e-4 with a systematic shrinkage bias.
 // TMA zero-fills out-of-range rows/columns, so ragged m and n need no special cases.  X must have
 // a 16-byte aligned row pitch (the caller pads when n % 4 != 0).
 #include "common.cuh"
@@ -17,6 +26,7 @@
 #include "tc_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace rnmf_gpu {
@@ -24,172 +34,259 @@ namespace rnmf_gpu {
 namespace {
 
 constexpr int kTcThreads = 256;
+// 3xTF32: six split warps (2-3 and 8-11) produce the lo tile while 0 / 1 / 4-7 keep their roles
+constexpr int kTcThreadsX3 = 384;
+constexpr int kSplitThreads = 192;
+template <bool X3>
+constexpr int tc_threads() { return X3 ? kTcThreadsX3 : kTcThreads; }
 constexpr int kBM = 128;          // rows per tile (UMMA M)
-constexpr int kBK = 32;           // fp32 columns per stage = one 128 B swizzle row
-constexpr int kXTileBytes = kBM * kBK * 4;
+constexpr int kBK = 32;           // fp32 K elements per stage = one 128 B swizzle row
+constexpr int kXTileBytes = kBM * kBK * 4;  // 16 KB: one X stage (either kernel)
+constexpr int kLoSlots = 3;       // 3xTF32 lo-tile ring
+constexpr int kSmemBudget = 220 * 1024;
 
+// 3xTF32 operand split.  hi = the raw fp32 word: kind::tf32 reads only the top 19 bits, i.e. it
+// truncates, so lo = rna_tf32(x - trunc_tf32(x)) is what the tensor core misses.  Only lo is
+// written; the X tile in the TMA ring is used unchanged as hi.
+__device__ __forceinline__ float tf32_lo(float v) {
+  return tc::tf32_hi(v - __uint_as_float(__float_as_uint(v) & 0xffffe000u));
+}
+
+// lo part of one X stage (N16 float4s) by kSplitThreads threads
+template <int N16>
+__device__ __forceinline__ void split_lo_tile(const float4* __restrict__ x4, float4* __restrict__ l4, int st) {
+#pragma unroll 4
+  for (int q = st; q < N16; q += kSplitThreads) {
+    const float4 v = x4[q];
+    l4[q] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+  }
+}
+
+// Shared layout of both kernels.  Ring stage = [X tile 16 KB][S^T hi slab][S^T lo slab (X3)], the
+// two slabs adjacent so that X_hi * [S_hi; S_lo]^T is ONE UMMA with N = 2 NPAD.  3xTF32 keeps the
+// lo X tiles in a separate 3-slot ring so the TMA ring stays deep.  TMEM accumulator buffer =
+// [X_hi S_hi | X_hi S_lo | X_lo S_hi] (3 NPAD columns; NPAD for 1xTF32), double-buffered when two
+// fit in the 512 columns.
 template <int NPAD, bool X3>
-struct XwCfg {
-  static constexpr int kSBytes = NPAD * kBK * 4;  // one S^T slab (hi or lo)
-  static constexpr int kStageBytes = kXTileBytes * (X3 ? 2 : 1) + kSBytes * (X3 ? 2 : 1);
-  static constexpr int kStages = std::min(6, (200 * 1024) / kStageBytes);
-  static constexpr int kTmemCols = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64) ? 64 : (2 * NPAD <= 128) ? 128 : 256;
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+struct TcCfg {
+  static constexpr int kSBytes = NPAD * kBK * 4;  // one S^T slab (NPAD rows x 128 B)
+  static constexpr int kStageBytes = kXTileBytes + kSBytes * (X3 ? 2 : 1);
+  static constexpr int kLoBytes = X3 ? kLoSlots * kXTileBytes : 0;
+  static constexpr int kStages = std::min(8, (kSmemBudget - kLoBytes - 2048) / kStageBytes);
+  static constexpr int kAccCols = X3 ? 3 * NPAD : NPAD;
+  static constexpr int kAccBufs = (2 * kAccCols <= 512) ? 2 : 1;
+  static constexpr int kUsedCols = kAccBufs * kAccCols;
+  static constexpr int kTmemCols = kUsedCols <= 32 ? 32 : kUsedCols <= 64 ? 64 : kUsedCols <= 128 ? 128
+                                   : kUsedCols <= 256 ? 256 : 512;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kLoBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(kStages >= 2, "ring too shallow");
+  static_assert(kUsedCols <= 512, "TMEM");
 };
 
-struct XwParams {
-  int64_t m, n;
-  int c;
-  float* y;
-  int64_t ldy;
-};
-
 template <int NPAD, bool X3>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_xw_kernel(const __grid_constant__ CUtensorMap tmX,
-                                                              const __grid_constant__ CUtensorMap tmShi,
-                                                              const __grid_constant__ CUtensorMap tmSlo, XwParams p) {
-  using C = XwCfg<NPAD, X3>;
-  constexpr int S = C::kStages;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  auto xs = [&](int s) { return smem + size_t(s) * C::kStageBytes; };
-  auto xlo = [&](int s) { return smem + size_t(s) * C::kStageBytes + kXTileBytes; };
-  auto shi = [&](int s) { return smem + size_t(s) * C::kStageBytes + kXTileBytes * (X3 ? 2 : 1); };
-  auto slo = [&](int s) { return shi(s) + C::kSBytes; };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::kStageBytes);
-  uint64_t* full = bars;
-  uint64_t* split = bars + S;
-  uint64_t* empty = bars + 2 * S;
-  uint64_t* tfull = bars + 3 * S;
-  uint64_t* tempty = bars + 3 * S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntiles = ceil_div(p.m, kBM);
-  const int nk = int(ceil_div(p.n, kBK));
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
+struct TcSmem {
+  using C = TcCfg<NPAD, X3>;
+  unsigned char* base;
+  uint64_t *full, *empty, *lofull, *loempty, *tfull, *tempty;
+  uint32_t* tmem_slot;
+  __device__ explicit TcSmem(unsigned char* raw) {
+    base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + size_t(C::kStages) * C::kStageBytes + C::kLoBytes);
+    full = bars;
+    empty = full + C::kStages;
+    lofull = empty + C::kStages;
+    loempty = lofull + kLoSlots;
+    tfull = loempty + kLoSlots;
+    tempty = tfull + 2;
+    tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  }
+  __device__ unsigned char* x(int s) const { return base + size_t(s) * C::kStageBytes; }
+  __device__ unsigned char* shi(int s) const { return x(s) + kXTileBytes; }
+  __device__ unsigned char* slo(int s) const { return shi(s) + C::kSBytes; }
+  __device__ unsigned char* lo(int j) const { return base + size_t(C::kStages) * C::kStageBytes + size_t(j) * kXTileBytes; }
+  __device__ void init(int split_count) const {
+    for (int s = 0; s < C::kStages; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&split[s], 64);
       tc::mbar_init(&empty[s], 1);
+    }
+    for (int j = 0; j < kLoSlots; ++j) {
+      tc::mbar_init(&lofull[j], split_count);
+      tc::mbar_init(&loempty[j], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], 128);
     }
     tc::fence_mbar_init();
+  }
+};
+
+// One K stage of UMMAs into accumulator buffer d.  a_desc(k, base) builds the A descriptor of
+// k-step k (A = X tile hi or lo); B is K-major SW128 in either kernel.
+template <int NPAD, bool X3, bool A_MN, typename ADesc>
+__device__ __forceinline__ void issue_stage(uint32_t d, uint32_t xa, uint32_t la, uint32_t ba, bool fresh, ADesc a_desc) {
+  constexpr uint32_t idesc1 = tc::make_idesc_tf32(NPAD, A_MN, false);
+  constexpr uint32_t idesc2 = tc::make_idesc_tf32(2 * NPAD, A_MN, false);
+#pragma unroll
+  for (int k = 0; k < kBK / 8; ++k) {
+    const uint64_t adesc = a_desc(xa, k);
+    const uint64_t bdesc = tc::make_sdesc(ba + k * 32, 16, 1024);
+    const uint32_t acc = (fresh && k == 0) ? 0u : 1u;
+    if (X3) {
+      tc::umma_tf32(d, adesc, bdesc, idesc2, acc);                                 // X_hi [S_hi; S_lo]
+      tc::umma_tf32(d + 2 * NPAD, a_desc(la, k), bdesc, idesc1, acc);              // X_lo S_hi
+    } else {
+      tc::umma_tf32(d, adesc, bdesc, idesc1, acc);
+    }
+  }
+}
+
+// Epilogue: add one accumulator buffer (this warp's 32 lanes) into the fp32 registers a[].
+// Small terms first: a += hihi + (hi*lo_S + lo_X*hi), each add rounded to nearest.
+template <int NPAD, bool X3>
+__device__ __forceinline__ void drain_acc(uint32_t taddr, float (&a)[NPAD]) {
+#pragma unroll
+  for (int cc = 0; cc < NPAD / 16; ++cc) {
+    uint32_t r0[16];
+    tc::tmem_ld_32x32b_x16(taddr + cc * 16, r0);
+    if (X3) {
+      uint32_t r1[16], r2[16];
+      tc::tmem_ld_32x32b_x16(taddr + NPAD + cc * 16, r1);
+      tc::tmem_ld_32x32b_x16(taddr + 2 * NPAD + cc * 16, r2);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        a[cc * 16 + q] += __uint_as_float(r0[q]) + (__uint_as_float(r1[q]) + __uint_as_float(r2[q]));
+    } else {
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) a[cc * 16 + q] += __uint_as_float(r0[q]);
+    }
+  }
+}
+
+struct XwParams {
+  int64_t m, n;
+  int c;
+  float* y;
+  int64_t ldy;
+  int chunk;  // K stages per TMEM accumulation chunk
+};
+
+// ------------------------------------------------------------------------------------------------
+// tc_xw: Y (m x c) = X (m x n) S (n x c); one 128-row tile per work unit, K = n.
+// The K loop is cut into chunks of p.chunk stages; each chunk starts a fresh TMEM accumulator that
+// the epilogue adds into fp32 registers, so the tensor core's truncating accumulation never runs
+// over more than p.chunk * 32 terms (tools/sketch_acc.cu measures the effect).
+template <int NPAD, bool X3>
+__global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                                    const __grid_constant__ CUtensorMap tmShi,
+                                                                    const __grid_constant__ CUtensorMap tmSlo, XwParams p) {
+  using C = TcCfg<NPAD, X3>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const TcSmem<NPAD, X3> sm(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = ceil_div(p.m, kBM);
+  const int nk = int(ceil_div(p.n, kBK));
+
+  if (threadIdx.x == 0) {
+    sm.init(kSplitThreads);
     tc::tma_prefetch(&tmX);
     tc::tma_prefetch(&tmShi);
     if (X3) tc::tma_prefetch(&tmSlo);
   }
-  if (warp == 1) tc::tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) tc::tmem_alloc<C::kTmemCols>(sm.tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = *sm.tmem_slot;
 
   if (warp == 0) {
     // ---------------- TMA producer
     if (tc::elect_one()) {
       uint32_t it = 0;
-      const uint32_t bytes = uint32_t(kXTileBytes + C::kSBytes * (X3 ? 2 : 1));
+      const uint32_t bytes = uint32_t(C::kStageBytes);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
-          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[s], bytes);
-          tc::tma_load_2d(xs(s), &tmX, &full[s], kc * kBK, int(t * kBM));
-          tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
-          if (X3) tc::tma_load_2d(slo(s), &tmSlo, &full[s], kc * kBK, 0);
+          tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&sm.full[s], bytes);
+          tc::tma_load_2d(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM));
+          tc::tma_load_2d(sm.shi(s), &tmShi, &sm.full[s], kc * kBK, 0);
+          if (X3) tc::tma_load_2d(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- UMMA issuer
-    constexpr uint32_t idesc = tc::make_idesc_tf32(NPAD, false, false);
-    uint32_t it = 0, ti = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
-      const int acc = int(ti & 1);
-      tc::mbar_wait(&tempty[acc], ((ti >> 1) & 1) ^ 1);
-      tc::tc_fence_after();
-      const uint32_t d = tmem_base + uint32_t(acc * NPAD);
+    uint32_t it = 0, ci = 0;
+    uint32_t d = tmem_base;
+    auto adesc = [](uint32_t base, int k) { return tc::make_sdesc(base + k * 32, 16, 1024); };
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int kc = 0; kc < nk; ++kc, ++it) {
-        const int s = int(it % S);
-        tc::mbar_wait(X3 ? &split[s] : &full[s], (it / S) & 1);
+        const int kin = kc % p.chunk;
+        const bool cend = (kin == p.chunk - 1) || (kc == nk - 1);
+        const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+        if (kin == 0) {
+          tc::mbar_wait(&sm.tempty[acc], ((C::kAccBufs == 2 ? ci >> 1 : ci) & 1) ^ 1);
+          tc::tc_fence_after();
+          d = tmem_base + uint32_t(acc * C::kAccCols);
+        }
+        const int s = int(it % S), j = int(it % kLoSlots);
+        tc::mbar_wait(&sm.full[s], (it / S) & 1);
+        if (X3) tc::mbar_wait(&sm.lofull[j], (it / kLoSlots) & 1);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          const uint32_t xa = tc::smem_u32(xs(s)), ba = tc::smem_u32(shi(s));
-#pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            const uint64_t adesc = tc::make_sdesc(xa + k * 32, 16, 1024);
-            const uint64_t bdesc = tc::make_sdesc(ba + k * 32, 16, 1024);
-            tc::umma_tf32(d, adesc, bdesc, idesc, (kc | k) != 0);
-            if (X3) {
-              const uint64_t bl = tc::make_sdesc(tc::smem_u32(slo(s)) + k * 32, 16, 1024);
-              const uint64_t al = tc::make_sdesc(tc::smem_u32(xlo(s)) + k * 32, 16, 1024);
-              tc::umma_tf32(d, adesc, bl, idesc, 1);
-              tc::umma_tf32(d, al, bdesc, idesc, 1);
-            }
-          }
-          tc::umma_commit(&empty[s]);
-          if (kc == nk - 1) tc::umma_commit(&tfull[acc]);
+          issue_stage<NPAD, X3, false>(d, tc::smem_u32(sm.x(s)), tc::smem_u32(sm.lo(j)), tc::smem_u32(sm.shi(s)),
+                                       kin == 0, adesc);
+          tc::umma_commit(&sm.empty[s]);
+          if (X3) tc::umma_commit(&sm.loempty[j]);
+          if (cend) tc::umma_commit(&sm.tfull[acc]);
         }
+        if (cend) ++ci;
         __syncwarp();
       }
     }
-  } else if (warp < 4) {
-    // ---------------- 3xTF32 split: X -> (hi in place, lo)
+  } else if (warp < 4 || warp >= 8) {
+    // ---------------- 3xTF32 split warps: lo tiles into their own ring
     if (X3) {
-      const int st = threadIdx.x - 64;  // 0..63
+      const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;  // 0..191
       uint32_t it = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = int(it % S);
-          tc::mbar_wait(&full[s], (it / S) & 1);
-          float4* x4 = reinterpret_cast<float4*>(xs(s));
-          float4* l4 = reinterpret_cast<float4*>(xlo(s));
-#pragma unroll 4
-          for (int q = st; q < kXTileBytes / 16; q += 64) {
-            float4 v = x4[q], lo;
-            float h;
-            h = tc::tf32_hi(v.x), lo.x = v.x - h, v.x = h;
-            h = tc::tf32_hi(v.y), lo.y = v.y - h, v.y = h;
-            h = tc::tf32_hi(v.z), lo.z = v.z - h, v.z = h;
-            h = tc::tf32_hi(v.w), lo.w = v.w - h, v.w = h;
-            x4[q] = v;
-            l4[q] = lo;
-          }
+          const int s = int(it % S), j = int(it % kLoSlots);
+          tc::mbar_wait(&sm.full[s], (it / S) & 1);
+          tc::mbar_wait(&sm.loempty[j], ((it / kLoSlots) & 1) ^ 1);
+          split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(sm.x(s)), reinterpret_cast<float4*>(sm.lo(j)), st);
           tc::fence_proxy_async_smem();
-          tc::mbar_arrive(&split[s]);
+          tc::mbar_arrive(&sm.lofull[j]);
         }
       }
     }
   } else {
-    // ---------------- epilogue: TMEM -> registers -> Y
+    // ---------------- epilogue: TMEM chunks -> fp32 registers -> Y
     const int sub = warp & 3;
-    uint32_t ti = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
-      const int acc = int(ti & 1);
-      tc::mbar_wait(&tfull[acc], (ti >> 1) & 1);
-      tc::tc_fence_after();
+    const int nch = (nk + p.chunk - 1) / p.chunk;
+    uint32_t ci = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t row = t * kBM + sub * 32 + lane;
-      const uint32_t taddr = tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * NPAD);
+      float a[NPAD];
 #pragma unroll
-      for (int cc = 0; cc < NPAD / 16; ++cc) {
-        uint32_t r[16];
-        tc::tmem_ld_32x32b_x16(taddr + cc * 16, r);
-        tc::tmem_ld_wait();
-        if (row < p.m) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int col = cc * 16 + q;
-            if (col < p.c) p.y[row * p.ldy + col] = __uint_as_float(r[q]);
-          }
-        }
+      for (int q = 0; q < NPAD; ++q) a[q] = 0.f;
+      for (int ch = 0; ch < nch; ++ch, ++ci) {
+        const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+        tc::mbar_wait(&sm.tfull[acc], (C::kAccBufs == 2 ? ci >> 1 : ci) & 1);
+        tc::tc_fence_after();
+        drain_acc<NPAD, X3>(tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * C::kAccCols), a);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&sm.tempty[acc]);
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&tempty[acc]);
+      if (row < p.m) {
+#pragma unroll
+        for (int q = 0; q < NPAD; ++q)
+          if (q < p.c) p.y[row * p.ldy + q] = a[q];
+      }
     }
   }
   tc::tc_fence_before();
@@ -203,70 +300,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xw_kernel(const __grid_const
 // ------------------------------------------------------------------------------------------------
 // tc_xtw: part[split] (n x c) = X[rows of split]^T (n x m_s) * S[rows of split] (m_s x c)
 //   A = X^T tile: M = 128 X columns (MN-major: four 32-column TMA boxes, LBO = 4 KB),
-//       K = 32 X rows per stage (SBO = 1024 B per 8 rows)
+//       K = 32 X rows per stage (SBO = 512 B per 4 rows, SW128_BASE32B)
 //   B = S^T slab (N = NPAD rows of the transposed small operand, K-major)
 // One work unit = (128-column tile, row split); units are distributed over persistent CTAs.
-template <int NPAD, bool X3 = false>
-struct XtwCfg {
-  static constexpr int kXBytes = 128 * kBK * 4;  // 32 rows x 128 cols
-  static constexpr int kSBytes = NPAD * kBK * 4;
-  static constexpr int kStageBytes = (kXBytes + kSBytes) * (X3 ? 2 : 1);
-  static constexpr int kStages = std::min(6, (200 * 1024) / kStageBytes);
-  static constexpr int kTmemCols = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64) ? 64 : (2 * NPAD <= 128) ? 128 : 256;
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 + 256;
-};
-
 struct XtwParams {
   int64_t m, n;
   int c;
   int splits;
   float* part;  // splits x n x c
+  int chunk;    // K stages (32 rows each) per TMEM accumulation chunk
 };
 
 template <int NPAD, bool X3>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_constant__ CUtensorMap tmX,
-                                                               const __grid_constant__ CUtensorMap tmSt,
-                                                               const __grid_constant__ CUtensorMap tmStLo, XtwParams p) {
-  using C = XtwCfg<NPAD, X3>;
+__global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                                     const __grid_constant__ CUtensorMap tmSt,
+                                                                     const __grid_constant__ CUtensorMap tmStLo, XtwParams p) {
+  using C = TcCfg<NPAD, X3>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  auto xs = [&](int s) { return smem + size_t(s) * C::kStageBytes; };
-  auto ss = [&](int s) { return smem + size_t(s) * C::kStageBytes + C::kXBytes; };
-  auto xl = [&](int s) { return smem + size_t(s) * C::kStageBytes + C::kXBytes + C::kSBytes; };
-  auto sl = [&](int s) { return xl(s) + C::kXBytes; };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::kStageBytes);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + S;
-  uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = bars + 2 * S + 2;
-  uint64_t* split = bars + 2 * S + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
-
+  const TcSmem<NPAD, X3> sm(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ctiles = ceil_div(p.n, 128);
   const int64_t units = ctiles * p.splits;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
-      tc::mbar_init(&split[s], 64);
-    }
-    for (int a = 0; a < 2; ++a) {
-      tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 128);
-    }
-    tc::fence_mbar_init();
+    sm.init(kSplitThreads);
     tc::tma_prefetch(&tmX);
     tc::tma_prefetch(&tmSt);
     if (X3) tc::tma_prefetch(&tmStLo);
   }
-  if (warp == 1) tc::tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) tc::tmem_alloc<C::kTmemCols>(sm.tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = *sm.tmem_slot;
 
   // split boundaries on 32-row stage boundaries, so no stage straddles two splits
   const int64_t mstages = ceil_div(p.m, kBK);
@@ -285,112 +352,104 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
         unit_rows(u, r0, r1);
         for (int64_t r = r0; r < r1; r += kBK, ++it) {
           const int s = int(it % S);
-          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kXBytes + C::kSBytes * (X3 ? 2 : 1)));
+          tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(C::kStageBytes));
 #pragma unroll
-          for (int b = 0; b < 4; ++b) tc::tma_load_2d(xs(s) + b * 4096, &tmX, &full[s], int(ct * 128 + b * 32), int(r));
-          tc::tma_load_2d(ss(s), &tmSt, &full[s], int(r), 0);
-          if (X3) tc::tma_load_2d(sl(s), &tmStLo, &full[s], int(r), 0);
+          for (int b = 0; b < 4; ++b) tc::tma_load_2d(sm.x(s) + b * 4096, &tmX, &sm.full[s], int(ct * 128 + b * 32), int(r));
+          tc::tma_load_2d(sm.shi(s), &tmSt, &sm.full[s], int(r), 0);
+          if (X3) tc::tma_load_2d(sm.slo(s), &tmStLo, &sm.full[s], int(r), 0);
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = tc::make_idesc_tf32(NPAD, true, false);
-    uint32_t it = 0, ti = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ti) {
+    uint32_t it = 0, ci = 0;
+    uint32_t d = tmem_base;
+    // MN-major A (SW128_BASE32B): LBO = 4 KB between 32-column boxes, SBO = 512 B per 4 rows
+    auto adesc = [](uint32_t base, int k) { return tc::make_sdesc(base + k * 1024, 4096, 512, tc::kLayoutSW128Base32B); };
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       int64_t r0, r1;
       unit_rows(u, r0, r1);
-      const int acc = int(ti & 1);
-      tc::mbar_wait(&tempty[acc], ((ti >> 1) & 1) ^ 1);
-      tc::tc_fence_after();
-      const uint32_t d = tmem_base + uint32_t(acc * NPAD);
-      bool first = true;
+      if (r0 >= r1) {  // empty split: still hand an (all-zero) chunk to the epilogue
+        const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+        tc::mbar_wait(&sm.tempty[acc], ((C::kAccBufs == 2 ? ci >> 1 : ci) & 1) ^ 1);
+        if (tc::elect_one()) tc::mbar_arrive(&sm.tfull[acc]);
+        ++ci;
+        __syncwarp();
+        continue;
+      }
+      int kin = 0;
       for (int64_t r = r0; r < r1; r += kBK, ++it) {
-        const int s = int(it % S);
-        tc::mbar_wait(X3 ? &split[s] : &full[s], (it / S) & 1);
+        const bool cend = (kin == p.chunk - 1) || (r + kBK >= r1);
+        const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+        if (kin == 0) {
+          tc::mbar_wait(&sm.tempty[acc], ((C::kAccBufs == 2 ? ci >> 1 : ci) & 1) ^ 1);
+          tc::tc_fence_after();
+          d = tmem_base + uint32_t(acc * C::kAccCols);
+        }
+        const int s = int(it % S), j = int(it % kLoSlots);
+        tc::mbar_wait(&sm.full[s], (it / S) & 1);
+        if (X3) tc::mbar_wait(&sm.lofull[j], (it / kLoSlots) & 1);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          const uint32_t xa = tc::smem_u32(xs(s)), ba = tc::smem_u32(ss(s));
-#pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            // MN-major A (SW128_BASE32B): LBO = 4 KB between 32-column boxes, SBO = 512 B per 4 rows
-            const uint64_t adesc = tc::make_sdesc(xa + k * 1024, 4096, 512, tc::kLayoutSW128Base32B);
-            const uint64_t bdesc = tc::make_sdesc(ba + k * 32, 16, 1024);
-            tc::umma_tf32(d, adesc, bdesc, idesc, (first && k == 0) ? 0u : 1u);
-            if (X3) {
-              const uint64_t al = tc::make_sdesc(tc::smem_u32(xl(s)) + k * 1024, 4096, 512, tc::kLayoutSW128Base32B);
-              const uint64_t bl = tc::make_sdesc(tc::smem_u32(sl(s)) + k * 32, 16, 1024);
-              tc::umma_tf32(d, adesc, bl, idesc, 1);
-              tc::umma_tf32(d, al, bdesc, idesc, 1);
-            }
-          }
-          tc::umma_commit(&empty[s]);
-          if (r + kBK >= r1) tc::umma_commit(&tfull[acc]);
+          issue_stage<NPAD, X3, true>(d, tc::smem_u32(sm.x(s)), tc::smem_u32(sm.lo(j)), tc::smem_u32(sm.shi(s)),
+                                      kin == 0, adesc);
+          tc::umma_commit(&sm.empty[s]);
+          if (X3) tc::umma_commit(&sm.loempty[j]);
+          if (cend) tc::umma_commit(&sm.tfull[acc]);
         }
-        first = false;
-        __syncwarp();
-      }
-      if (r0 >= r1) {  // empty split: still hand an (all-zero) accumulator to the epilogue
-        if (tc::elect_one()) tc::mbar_arrive(&tfull[acc]);
+        if (cend) {
+          ++ci;
+          kin = 0;
+        } else {
+          ++kin;
+        }
         __syncwarp();
       }
     }
-  } else if (warp < 4) {
-    if (X3) {  // 3xTF32 split of the X tile (elementwise, so the swizzled layout is irrelevant)
-      const int st = threadIdx.x - 64;
+  } else if (warp < 4 || warp >= 8) {
+    if (X3) {  // 3xTF32 lo tiles (elementwise, so the swizzled layout is irrelevant)
+      const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t r0, r1;
         unit_rows(u, r0, r1);
         for (int64_t r = r0; r < r1; r += kBK, ++it) {
-          const int s = int(it % S);
-          tc::mbar_wait(&full[s], (it / S) & 1);
-          float4* x4 = reinterpret_cast<float4*>(xs(s));
-          float4* l4 = reinterpret_cast<float4*>(xl(s));
-#pragma unroll 4
-          for (int q = st; q < C::kXBytes / 16; q += 64) {
-            float4 v = x4[q], lo;
-            float h;
-            h = tc::tf32_hi(v.x), lo.x = v.x - h, v.x = h;
-            h = tc::tf32_hi(v.y), lo.y = v.y - h, v.y = h;
-            h = tc::tf32_hi(v.z), lo.z = v.z - h, v.z = h;
-            h = tc::tf32_hi(v.w), lo.w = v.w - h, v.w = h;
-            x4[q] = v;
-            l4[q] = lo;
-          }
+          const int s = int(it % S), j = int(it % kLoSlots);
+          tc::mbar_wait(&sm.full[s], (it / S) & 1);
+          tc::mbar_wait(&sm.loempty[j], ((it / kLoSlots) & 1) ^ 1);
+          split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(sm.x(s)), reinterpret_cast<float4*>(sm.lo(j)), st);
           tc::fence_proxy_async_smem();
-          tc::mbar_arrive(&split[s]);
+          tc::mbar_arrive(&sm.lofull[j]);
         }
       }
     }
   } else {
     const int sub = warp & 3;
-    uint32_t ti = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ti) {
+    uint32_t ci = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t ct = u / p.splits, sp = u % p.splits;
       int64_t r0, r1;
       unit_rows(u, r0, r1);
-      const int acc = int(ti & 1);
-      tc::mbar_wait(&tfull[acc], (ti >> 1) & 1);
-      tc::tc_fence_after();
+      const int64_t nst = (r1 - r0) / kBK;
+      const int64_t nch = r0 < r1 ? (nst + p.chunk - 1) / p.chunk : 1;
       const int64_t col = ct * 128 + sub * 32 + lane;  // X column = output row of P
-      const uint32_t taddr = tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * NPAD);
-      float* out = p.part + (sp * p.n + col) * p.c;
+      float a[NPAD];
 #pragma unroll
-      for (int cc = 0; cc < NPAD / 16; ++cc) {
-        uint32_t rr[16];
-        tc::tmem_ld_32x32b_x16(taddr + cc * 16, rr);
-        tc::tmem_ld_wait();
-        if (col < p.n) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int j = cc * 16 + q;
-            if (j < p.c) out[j] = (r0 < r1) ? __uint_as_float(rr[q]) : 0.f;
-          }
-        }
+      for (int q = 0; q < NPAD; ++q) a[q] = 0.f;
+      for (int64_t ch = 0; ch < nch; ++ch, ++ci) {
+        const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+        tc::mbar_wait(&sm.tfull[acc], (C::kAccBufs == 2 ? ci >> 1 : ci) & 1);
+        tc::tc_fence_after();
+        if (r0 < r1) drain_acc<NPAD, X3>(tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * C::kAccCols), a);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&sm.tempty[acc]);
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&tempty[acc]);
+      if (col < p.n) {
+        float* out = p.part + (sp * p.n + col) * p.c;
+#pragma unroll
+        for (int q = 0; q < NPAD; ++q)
+          if (q < p.c) out[q] = a[q];
+      }
     }
   }
   tc::tc_fence_before();
@@ -401,7 +460,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_xtw_kernel(const __grid_cons
   }
 }
 
-// S (n x c, row-major, ld c) -> S^T hi / lo (npad x ldst, zero rows for j >= c and cols >= n)
+// S (n x c, row-major, ld c) -> S^T hi / lo (npad x ldst, zero rows for j >= c and cols >= n):
+// hi = rna_tf32(s) (exact tf32, the operand of 1xTF32 too), lo = rna_tf32(s - hi)
 __global__ void prep_st_kernel(const float* __restrict__ s, int64_t n, int c, int npad, int64_t ldst,
                                float* __restrict__ st_hi, float* __restrict__ st_lo) {
   const int64_t total = int64_t(npad) * ldst;
@@ -411,7 +471,7 @@ __global__ void prep_st_kernel(const float* __restrict__ s, int64_t n, int c, in
     const float v = (j < c && kk < n) ? s[kk * c + j] : 0.f;
     const float h = tc::tf32_hi(v);
     st_hi[e] = h;
-    st_lo[e] = v - h;
+    st_lo[e] = tc::tf32_hi(v - h);
   }
 }
 
@@ -449,19 +509,30 @@ CUtensorMap make_map_2d(const float* base, int64_t rows, int64_t cols, int64_t p
   return m;
 }
 
+// K stages (32 columns / rows each) per TMEM accumulation chunk; RNMF_TC_CHUNK overrides.
+int g_tc_chunk = 0;
+int tc_chunk_stages() {
+  if (g_tc_chunk <= 0) {
+    const char* e = std::getenv("RNMF_TC_CHUNK");
+    const int c = e ? std::atoi(e) : 0;
+    g_tc_chunk = c > 0 ? c : 2;
+  }
+  return g_tc_chunk;
+}
+
 template <int NPAD, bool X3>
 void tc_xw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
                   int64_t ldst, int c, float* y, int sm_count, cudaStream_t stream) {
-  using C = XwCfg<NPAD, X3>;
+  using C = TcCfg<NPAD, X3>;
   const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBM);
   const CUtensorMap mh = make_map_2d(st_hi, NPAD, n, ldst, NPAD);
   const CUtensorMap ml = make_map_2d(st_lo, NPAD, n, ldst, NPAD);
-  XwParams p{m, n, c, y, c};
+  XwParams p{m, n, c, y, c, tc_chunk_stages()};
   auto f = tc_xw_kernel<NPAD, X3>;
   RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
   const int64_t ntiles = ceil_div(m, kBM);
   const int grid = int(std::min<int64_t>(ntiles, sm_count));
-  f<<<grid, kTcThreads, C::kSmem, stream>>>(mx, mh, ml, p);
+  f<<<grid, tc_threads<X3>(), C::kSmem, stream>>>(mx, mh, ml, p);
   RNMF_CUDA_LAUNCH();
 }
 
@@ -469,16 +540,16 @@ void tc_xw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float
 template <int NPAD, bool X3>
 void tc_xtw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int64_t ldst,
                    int c, float* part, int splits, int sm_count, cudaStream_t stream) {
-  using C = XtwCfg<NPAD, X3>;
+  using C = TcCfg<NPAD, X3>;
   const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);  // 32 x 32 boxes
   const CUtensorMap ms = make_map_2d(st, NPAD, m, ldst, NPAD);  // S^T: NPAD rows x m
   const CUtensorMap ml = make_map_2d(X3 ? st_lo : st, NPAD, m, ldst, NPAD);
-  XtwParams p{m, n, c, splits, part};
+  XtwParams p{m, n, c, splits, part, tc_chunk_stages()};
   auto f = tc_xtw_kernel<NPAD, X3>;
   RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
   const int64_t units = ceil_div(n, 128) * splits;
   const int grid = int(std::min<int64_t>(units, sm_count));
-  f<<<grid, kTcThreads, C::kSmem, stream>>>(mx, ms, ml, p);
+  f<<<grid, tc_threads<X3>(), C::kSmem, stream>>>(mx, ms, ml, p);
   RNMF_CUDA_LAUNCH();
 }
 
@@ -530,6 +601,8 @@ namespace {
 }  // namespace
 
 int tc_npad(int c) { return int(ceil_div(c, 16) * 16); }
+
+void tc_set_chunk(int stages) { g_tc_chunk = stages; }
 
 int64_t tc_st_pitch(int64_t n) { return ceil_div(n, 32) * 32; }
 

@@ -1,0 +1,57 @@
+"""GPU parity of math_mode TF32X3 (X-streaming sketch GEMMs on tcgen05 tensor cores, 3xTF32 split
+with chunked TMEM accumulation promoted to fp32 registers) against the fp64 oracle, at the same
+fp32 tolerances as the EXACT (FFMA) verification mode: per-record trace within 1e-3 relative and
+final rel_err within 1e-4 absolute (BASELINE.json north_star).  EXACT stays the verification mode;
+these tests show the tensor-core sketch does not loosen the bar.
+
+Sizes cover both tcgen05 kernels' code paths: several 128-row tiles and ragged tails (m, n not
+multiples of 128 / 32), several K chunks (n > 64, rows per split > 64), c = l below, at and above
+one 16-column UMMA step.
+"""
+import numpy as np
+import pytest
+
+from paper_1711_02037_b200 import workloads
+
+from test_gpu_parity import F32_FINAL_ATOL, F32_TRACE_RTOL, _odict, assert_trace_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,n,k,p", [(700, 300, 6, 8), (2051, 517, 10, 10), (4100, 1000, 16, 20), (333, 1200, 5, 11)])
+def test_tf32x3_fit_parity(gpu, oracle, m, n, k, p):
+    x = oracle.synth_lowrank(m, n, k, 0.05, 100 + m)
+    o = gpu.SolverOptions(rank=k, max_iter=30, tol=1e-300, oversampling=p, power_iterations=2, seed=7)
+    l = min(k + p, m, n)
+    om, w0, h0 = workloads.injected_inputs(2, m, n, k, l)
+    ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    o.math_mode = gpu.MathMode.TF32x3
+    res = gpu.rhals_fit(x.astype(np.float32), o, omega=om, w0=w0, h0=h0)
+    assert_trace_close(res.trace, ref.trace, F32_TRACE_RTOL, F32_FINAL_ATOL,
+                       fields=("rel_err", "objective_compressed", "objective", "pgrad", "pgrad_full"))
+
+
+def test_tf32x3_faces_config_parity(gpu, oracle):
+    """BASELINE config 2 shape and data (faces-like 32256 x 2410, k 16, p 20, q 2), 30 sweeps."""
+    x = workloads.faces_matrix(0)
+    m, n = x.shape
+    o = gpu.SolverOptions(rank=16, max_iter=30, tol=1e-300, oversampling=20, power_iterations=2, seed=0)
+    om, w0, h0 = workloads.injected_inputs(0, m, n, 16, 36)
+    ref = oracle.rhals_fit(x.astype(np.float64), _odict(o), omega=om, w0=w0, h0=h0)
+    o.math_mode = gpu.MathMode.TF32x3
+    res = gpu.rhals_fit(x, o, omega=om, w0=w0, h0=h0)
+    assert_trace_close(res.trace, ref.trace, F32_TRACE_RTOL, F32_FINAL_ATOL,
+                       fields=("rel_err", "objective_compressed", "objective", "pgrad", "pgrad_full"))
+
+
+def test_tf32x3_rqb_projector(gpu, oracle):
+    """The tensor-core sketch spans the same subspace as the fp64 oracle's (QQ^T X agrees)."""
+    x = oracle.synth_lowrank(1500, 700, 12, 0.05, 5)
+    om = np.random.default_rng(3).standard_normal((700, 20))
+    r = gpu.rqb(x.astype(np.float32), gpu.SketchOptions(target_rank=12, oversampling=8, power_iterations=2), omega=om,
+                math_mode=gpu.MathMode.TF32x3)
+    qo, bo = oracle.rqb(x, 12, 8, 2, omega=om)
+    q = r.q.astype(np.float64)
+    b = r.b.astype(np.float64)
+    np.testing.assert_allclose(q.T @ q, np.eye(20), atol=1e-5)
+    np.testing.assert_allclose(q @ b, qo @ bo, atol=2e-5 * np.abs(x).max())

@@ -83,7 +83,7 @@ def main(src, dst, cfg):
                     f"{cfg} --steps 1 --warmup 3 (cold-cache, serialised: compare shares)\n")
             f.write(launch_summary(lp))
     kernels = {}
-    for name in ("rhals_sweeps_kernel", "metrics_kernel", "xw_kernel", "xtw_kernel"):
+    for name in ("rhals_sweeps_kernel", "metrics_kernel", "tc_xw_kernel", "tc_xtw_kernel", "xw_tma_kernel", "xtw_tma_kernel"):
         rep = os.path.join(src, f"{name}_{cfg}.ncu-rep")
         if os.path.exists(rep):
             kernels[name] = kernel_metrics(rep)
@@ -102,7 +102,8 @@ def main(src, dst, cfg):
         allt = json.load(open(lt))
     except Exception:
         allt = {}
-    sk = [kernels[k]["dram_bytes"] for k in ("xw_kernel", "xtw_kernel") if k in kernels]
+    sk = [kernels[k]["dram_bytes"] for k in ("tc_xw_kernel", "tc_xtw_kernel") if k in kernels] or \
+         [kernels[k]["dram_bytes"] for k in ("xw_tma_kernel", "xtw_tma_kernel") if k in kernels]
     allt[cfg] = {"source": os.path.join(os.path.basename(dst), f"ncu_{cfg}_kernels.json"),
                  "sketch_bytes_per_launch": sum(sk) / len(sk) if sk else None,
                  "kernels": {k: v["dram_bytes"] for k, v in kernels.items()}}

@@ -14,7 +14,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--fits", type=int, default=1)
     ap.add_argument("--iters", type=int, default=0, help="override sweep count")
-    ap.add_argument("--math", default="exact")
+    ap.add_argument("--math", default="tf32x3")
     args = ap.parse_args()
     import torch
 
