@@ -11,19 +11,20 @@
 //   warps 2-3, 8-11 (3xTF32 only) write lo = rna_tf32(X - trunc_tf32(X)) into a 3-slot lo ring;
 //                the raw X tile is the hi operand (kind::tf32 truncates), so per K step
 //                  D[0:2N)  = X_hi [S_hi; S_lo]^T   (one UMMA, N = 2 NPAD)
-//                  D[2N:3N) = X_lo S_hi^T
-//                and the big term never shares an accumulator with the small ones.
+//                  D[N:2N) += X_lo S_hi^T
+//                so the big term never shares an accumulator with the small ones.
 //   warps 4-7    epilogue: every chunk of p.chunk stages lands in a fresh TMEM buffer that the
 //                epilogue adds into fp32 registers (round-to-nearest), which bounds the tensor
 //                core's truncating accumulation to p.chunk * 32 terms.  Measured on B200
-//                (tools/sketch_acc.cu): 3xTF32 with 64-term chunks is as accurate as the FFMA
-//                kernels (rms error 7e-7 vs 8e-7 of the result), where whole-K accumulation was
+//                (tools/sketch_acc.cu): 3xTF32 with 128-term chunks is more accurate than the FFMA
+//                kernels (rms error 3-4e-7 vs 8e-7 - 2e-6 of the result), where whole-K accumulation was
 //                2e-5 - 1e-4 with a systematic shrinkage bias.
 // TMA zero-fills out-of-range rows/columns, so ragged m and n need no special cases.  X must have
 // a 16-byte aligned row pitch (the caller pads when n % 4 != 0).
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
+#include "tc_metrics.h"
 
 #include <algorithm>
 #include <cstdlib>
@@ -42,8 +43,14 @@ constexpr int tc_threads() { return X3 ? kTcThreadsX3 : kTcThreads; }
 constexpr int kBM = 128;          // rows per tile (UMMA M)
 constexpr int kBK = 32;           // fp32 K elements per stage = one 128 B swizzle row
 constexpr int kXTileBytes = kBM * kBK * 4;  // 16 KB: one X stage (either kernel)
-constexpr int kLoSlots = 3;       // 3xTF32 lo-tile ring
-constexpr int kSmemBudget = 220 * 1024;
+#ifndef RNMF_TC_LO_SLOTS
+#define RNMF_TC_LO_SLOTS 3
+#endif
+#ifndef RNMF_TC_SMEM_KB
+#define RNMF_TC_SMEM_KB 220
+#endif
+constexpr int kLoSlots = RNMF_TC_LO_SLOTS;  // 3xTF32 lo-tile ring
+constexpr int kSmemBudget = RNMF_TC_SMEM_KB * 1024;
 
 // 3xTF32 operand split.  hi = the raw fp32 word: kind::tf32 reads only the top 19 bits, i.e. it
 // truncates, so lo = rna_tf32(x - trunc_tf32(x)) is what the tensor core misses.  Only lo is
@@ -52,28 +59,48 @@ __device__ __forceinline__ float tf32_lo(float v) {
   return tc::tf32_hi(v - __uint_as_float(__float_as_uint(v) & 0xffffe000u));
 }
 
-// lo part of one X stage (N16 float4s) by kSplitThreads threads
+__device__ __forceinline__ uint32_t tf32_lo_bits(uint32_t u) {
+  // d = x - trunc_tf32(x) (exact), then round d to tf32, nearest with ties away (= cvt.rna.tf32)
+  const uint32_t d = __float_as_uint(__uint_as_float(u) - __uint_as_float(u & 0xffffe000u));
+  return (d + 0x1000u) & 0xffffe000u;
+}
+
+// lo part of one X stage (N16 float4s) by kSplitThreads threads: explicit shared-space vector
+// loads / stores (the tile pointers are generic in C++), all loads of a thread issued first
 template <int N16>
 __device__ __forceinline__ void split_lo_tile(const float4* __restrict__ x4, float4* __restrict__ l4, int st) {
-#pragma unroll 4
-  for (int q = st; q < N16; q += kSplitThreads) {
-    const float4 v = x4[q];
-    l4[q] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+  constexpr int kIt = (N16 + kSplitThreads - 1) / kSplitThreads;
+  const uint32_t xs = tc::smem_u32(x4), ls = tc::smem_u32(l4);
+  uint32_t v[kIt][4];
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int q = st + i * kSplitThreads;
+    if (q < N16)
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3])
+                   : "r"(xs + 16u * uint32_t(q)));
+  }
+#pragma unroll
+  for (int i = 0; i < kIt; ++i) {
+    const int q = st + i * kSplitThreads;
+    if (q < N16)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ls + 16u * uint32_t(q)), "r"(tf32_lo_bits(v[i][0])),
+                   "r"(tf32_lo_bits(v[i][1])), "r"(tf32_lo_bits(v[i][2])), "r"(tf32_lo_bits(v[i][3]))
+                   : "memory");
   }
 }
 
 // Shared layout of both kernels.  Ring stage = [X tile 16 KB][S^T hi slab][S^T lo slab (X3)], the
 // two slabs adjacent so that X_hi * [S_hi; S_lo]^T is ONE UMMA with N = 2 NPAD.  3xTF32 keeps the
 // lo X tiles in a separate 3-slot ring so the TMA ring stays deep.  TMEM accumulator buffer =
-// [X_hi S_hi | X_hi S_lo | X_lo S_hi] (3 NPAD columns; NPAD for 1xTF32), double-buffered when two
-// fit in the 512 columns.
+// [X_hi S_hi | X_hi S_lo + X_lo S_hi] (2 NPAD columns; NPAD for 1xTF32), double-buffered.
 template <int NPAD, bool X3>
 struct TcCfg {
   static constexpr int kSBytes = NPAD * kBK * 4;  // one S^T slab (NPAD rows x 128 B)
   static constexpr int kStageBytes = kXTileBytes + kSBytes * (X3 ? 2 : 1);
   static constexpr int kLoBytes = X3 ? kLoSlots * kXTileBytes : 0;
   static constexpr int kStages = std::min(8, (kSmemBudget - kLoBytes - 2048) / kStageBytes);
-  static constexpr int kAccCols = X3 ? 3 * NPAD : NPAD;
+  static constexpr int kAccCols = X3 ? 2 * NPAD : NPAD;
   static constexpr int kAccBufs = (2 * kAccCols <= 512) ? 2 : 1;
   static constexpr int kUsedCols = kAccBufs * kAccCols;
   static constexpr int kTmemCols = kUsedCols <= 32 ? 32 : kUsedCols <= 64 ? 64 : kUsedCols <= 128 ? 128
@@ -134,33 +161,44 @@ __device__ __forceinline__ void issue_stage(uint32_t d, uint32_t xa, uint32_t la
     const uint32_t acc = (fresh && k == 0) ? 0u : 1u;
     if (X3) {
       tc::umma_tf32(d, adesc, bdesc, idesc2, acc);                                 // X_hi [S_hi; S_lo]
-      tc::umma_tf32(d + 2 * NPAD, a_desc(la, k), bdesc, idesc1, acc);              // X_lo S_hi
+      tc::umma_tf32(d + NPAD, a_desc(la, k), bdesc, idesc1, 1u);                   // += X_lo S_hi (small terms)
     } else {
       tc::umma_tf32(d, adesc, bdesc, idesc1, acc);
     }
   }
 }
 
-// Epilogue: add one accumulator buffer (this warp's 32 lanes) into the fp32 registers a[].
-// Small terms first: a += hihi + (hi*lo_S + lo_X*hi), each add rounded to nearest.
+// Epilogue: add one accumulator buffer (this warp's 32 lanes) into the fp32 registers a[]:
+// a += hihi + small, each add rounded to nearest.
 template <int NPAD, bool X3>
 __device__ __forceinline__ void drain_acc(uint32_t taddr, float (&a)[NPAD]) {
+  if constexpr (X3 && NPAD % 32 == 0) {
+    // 32-column loads of both halves, one wait per 32 columns
 #pragma unroll
-  for (int cc = 0; cc < NPAD / 16; ++cc) {
-    uint32_t r0[16];
-    tc::tmem_ld_32x32b_x16(taddr + cc * 16, r0);
-    if (X3) {
-      uint32_t r1[16], r2[16];
-      tc::tmem_ld_32x32b_x16(taddr + NPAD + cc * 16, r1);
-      tc::tmem_ld_32x32b_x16(taddr + 2 * NPAD + cc * 16, r2);
+    for (int cc = 0; cc < NPAD / 32; ++cc) {
+      uint32_t r0[32], r1[32];
+      tc::tmem_ld_32x32b_x32(taddr + cc * 32, r0);
+      tc::tmem_ld_32x32b_x32(taddr + NPAD + cc * 32, r1);
       tc::tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        a[cc * 16 + q] += __uint_as_float(r0[q]) + (__uint_as_float(r1[q]) + __uint_as_float(r2[q]));
-    } else {
-      tc::tmem_ld_wait();
+      for (int q = 0; q < 32; ++q) a[cc * 32 + q] += __uint_as_float(r0[q]) + __uint_as_float(r1[q]);
+    }
+  } else {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) a[cc * 16 + q] += __uint_as_float(r0[q]);
+    for (int cc = 0; cc < NPAD / 16; ++cc) {
+      uint32_t r0[16];
+      tc::tmem_ld_32x32b_x16(taddr + cc * 16, r0);
+      if (X3) {
+        uint32_t r1[16];
+        tc::tmem_ld_32x32b_x16(taddr + NPAD + cc * 16, r1);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[cc * 16 + q] += __uint_as_float(r0[q]) + __uint_as_float(r1[q]);
+      } else {
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[cc * 16 + q] += __uint_as_float(r0[q]);
+      }
     }
   }
 }
@@ -515,7 +553,7 @@ int tc_chunk_stages() {
   if (g_tc_chunk <= 0) {
     const char* e = std::getenv("RNMF_TC_CHUNK");
     const int c = e ? std::atoi(e) : 0;
-    g_tc_chunk = c > 0 ? c : 2;
+    g_tc_chunk = c > 0 ? c : 4;
   }
   return g_tc_chunk;
 }
@@ -641,6 +679,334 @@ int launch_tc_xw(const float* x, int64_t m, int64_t n, int64_t ldx, const float*
       throw CudaError("tc_xw: column count above 128");
   }
 #undef RNMF_TC_XW
+  return 1;
+}
+
+
+// ================================================================================================
+// Full-space metrics on the tensor cores (tc_metrics.h).
+// ================================================================================================
+namespace {
+
+// tc_resid: per 128-row tile t, per 32-column stage: D (128 x 32) = W_t H(:, cols) by 3xTF32
+//   UMMAs (A = W tile hi / lo, K-major SW128, resident per tile; B = [H^T hi; H^T lo] slab, 2 x 32
+//   rows per 32-wide K atom, so X-free D[0:32) = W_hi H_hi, D[32:64) = W_hi H_lo + W_lo H_hi), then
+//   the epilogue reads its row of the X stage from shared memory and accumulates (x - wh)^2.
+// Roles: warp 0 TMA producer, warp 1 UMMA issuer, warps 4-7 epilogue (thread = row).
+constexpr int kRsThreads = 256;
+constexpr int kRsTmemBufs = 4;  // 64-column D buffers
+
+template <int KW>
+struct RsCfg {
+  static constexpr int kAtoms = KW / 32;
+  static constexpr int kWBytes = 2 * kAtoms * kXTileBytes;        // W_hi, W_lo atoms (128 rows each)
+  static constexpr int kHtAtomBytes = 2 * 32 * 128;                 // 32 hi rows + 32 lo rows
+  static constexpr int kStageBytes = kXTileBytes + kAtoms * kHtAtomBytes;
+  static constexpr int kStages = std::min(8, (kSmemBudget - kWBytes - 2048) / kStageBytes);
+  static constexpr size_t kSmem = size_t(kWBytes) + size_t(kStages) * kStageBytes + 1024 + 512;
+  static_assert(kStages >= 2, "ring too shallow");
+};
+
+template <int KW>
+__global__ void __launch_bounds__(kRsThreads, 1) tc_resid_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                                  const __grid_constant__ CUtensorMap tmWhi,
+                                                                  const __grid_constant__ CUtensorMap tmWlo,
+                                                                  const __grid_constant__ CUtensorMap tmHhi,
+                                                                  const __grid_constant__ CUtensorMap tmHlo, int64_t m,
+                                                                  int64_t n, double* __restrict__ part_obj) {
+  using C = RsCfg<KW>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* wsm = base;  // [hi atoms][lo atoms], 16 KB each
+  auto xst = [&](int s) { return base + C::kWBytes + size_t(s) * C::kStageBytes; };
+  auto hst = [&](int s) { return xst(s) + kXTileBytes; };  // atom a: hi rows at a * 8 KB, lo rows +4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::kWBytes + size_t(S) * C::kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + kRsTmemBufs;
+  uint64_t* wfull = tempty + kRsTmemBufs;
+  uint64_t* wempty = wfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+  double* red = reinterpret_cast<double*>(wempty + 2);  // 4 doubles
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = ceil_div(m, kBM);
+  const int nk = int(ceil_div(n, kBK));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1 + 4);  // UMMA commit (H slab read) + one arrival per epilogue warp (X read)
+    }
+    for (int b = 0; b < kRsTmemBufs; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 128);
+    }
+    tc::mbar_init(wfull, 1);
+    tc::mbar_init(wempty, 1);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmWhi);
+    tc::tma_prefetch(&tmWlo);
+    tc::tma_prefetch(&tmHhi);
+    tc::tma_prefetch(&tmHlo);
+  }
+  if (warp == 1) tc::tmem_alloc<256>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      uint32_t it = 0, ti = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+        // W tile (hi, lo) once per row tile, after the previous tile's UMMAs are done with it
+        tc::mbar_wait(wempty, (ti & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(wfull, uint32_t(C::kWBytes));
+#pragma unroll
+        for (int a = 0; a < C::kAtoms; ++a) {
+          tc::tma_load_2d(wsm + a * kXTileBytes, &tmWhi, wfull, a * 32, int(t * kBM));
+          tc::tma_load_2d(wsm + (C::kAtoms + a) * kXTileBytes, &tmWlo, wfull, a * 32, int(t * kBM));
+        }
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = int(it % S);
+          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
+          tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
+#pragma unroll
+          for (int a = 0; a < C::kAtoms; ++a) {
+            tc::tma_load_2d(hst(s) + a * C::kHtAtomBytes, &tmHhi, &full[s], a * 32, kc * kBK);
+            tc::tma_load_2d(hst(s) + a * C::kHtAtomBytes + 4096, &tmHlo, &full[s], a * 32, kc * kBK);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc1 = tc::make_idesc_tf32(32, false, false);
+    constexpr uint32_t idesc2 = tc::make_idesc_tf32(64, false, false);
+    uint32_t it = 0, ti = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+      tc::mbar_wait(wfull, ti & 1);
+      tc::tc_fence_after();
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = int(it % S), b = int(it % kRsTmemBufs);
+        tc::mbar_wait(&tempty[b], ((it / kRsTmemBufs) & 1) ^ 1);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint32_t d = tmem_base + uint32_t(b * 64);
+          const uint32_t wa = tc::smem_u32(wsm), ha = tc::smem_u32(hst(s));
+#pragma unroll
+          for (int kk = 0; kk < KW / 8; ++kk) {
+            const int a = kk / 4, ko = (kk % 4) * 32;
+            const uint64_t whi = tc::make_sdesc(wa + a * kXTileBytes + ko, 16, 1024);
+            const uint64_t wlo = tc::make_sdesc(wa + (C::kAtoms + a) * kXTileBytes + ko, 16, 1024);
+            const uint64_t hb = tc::make_sdesc(ha + a * C::kHtAtomBytes + ko, 16, 1024);  // 64 rows: hi | lo
+            tc::umma_tf32(d, whi, hb, idesc2, kk != 0);   // [W_hi H_hi | W_hi H_lo]
+            tc::umma_tf32(d + 32, wlo, hb, idesc1, 1u);   // += W_lo H_hi
+          }
+          tc::umma_commit(&empty[s]);
+          tc::umma_commit(&tfull[b]);
+          if (kc == nk - 1) tc::umma_commit(wempty);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int sub = warp & 3;
+    const int r = sub * 32 + lane;  // row within the tile
+    double acc = 0.0;
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = int(it % S), b = int(it % kRsTmemBufs);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&tfull[b], (it / kRsTmemBufs) & 1);
+        tc::tc_fence_after();
+        uint32_t d0[32], d1[32];
+        const uint32_t taddr = tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(b * 64);
+        tc::tmem_ld_32x32b_x32(taddr, d0);
+        tc::tmem_ld_32x32b_x32(taddr + 32, d1);
+        // row r of the SW128 X stage: 16-byte chunk c sits at chunk c ^ (r & 7)
+        const uint32_t xrow = tc::smem_u32(xst(s)) + uint32_t(r) * 128u;
+        float xv[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t v0, v1, v2, v3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)));
+          xv[4 * c] = __uint_as_float(v0), xv[4 * c + 1] = __uint_as_float(v1);
+          xv[4 * c + 2] = __uint_as_float(v2), xv[4 * c + 3] = __uint_as_float(v3);
+        }
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tempty[b]);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        float ss = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float e = xv[c] - (__uint_as_float(d0[c]) + __uint_as_float(d1[c]));
+          ss = fmaf(e, e, ss);
+        }
+        acc += double(ss);
+      }
+    }
+    // CTA partial: warp sums, fixed order over the 4 epilogue warps
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) red[sub] = acc;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) part_obj[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<256>(tmem_base);
+  }
+}
+
+__global__ void tc_resid_prep_kernel(const float* __restrict__ w, int64_t m, const float* __restrict__ h, int64_t n,
+                                     int k, int kw, int64_t npad, float* __restrict__ w_hi, float* __restrict__ w_lo,
+                                     float* __restrict__ ht_hi, float* __restrict__ ht_lo) {
+  const int64_t tw = m * kw, total = tw + npad * kw;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    float v;
+    float *hi, *lo;
+    if (e < tw) {
+      const int64_t i = e / kw;
+      const int j = int(e % kw);
+      v = j < k ? w[i * k + j] : 0.f;
+      hi = w_hi + e;
+      lo = w_lo + e;
+    } else {
+      const int64_t f = e - tw, c = f / kw;
+      const int j = int(f % kw);
+      v = (j < k && c < n) ? h[int64_t(j) * n + c] : 0.f;
+      hi = ht_hi + f;
+      lo = ht_lo + f;
+    }
+    const float vh = tc::tf32_hi(v);
+    *hi = vh;
+    *lo = tc::tf32_hi(v - vh);
+  }
+}
+
+__global__ void tc_prep_rows_kernel(const float* __restrict__ src, int c, int64_t n, int npad, int64_t ldst,
+                                    float* __restrict__ st_hi, float* __restrict__ st_lo) {
+  const int64_t total = int64_t(npad) * ldst;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int j = int(e / ldst);
+    const int64_t kk = e % ldst;
+    const float v = (j < c && kk < n) ? src[int64_t(j) * n + kk] : 0.f;
+    const float h = tc::tf32_hi(v);
+    st_hi[e] = h;
+    st_lo[e] = tc::tf32_hi(v - h);
+  }
+}
+
+// projected grad_W partial sums (projected_sq_norm, p/src/hals.cpp:55-65): one row per thread
+constexpr int kPgwThreads = 256;
+__global__ void __launch_bounds__(kPgwThreads) tc_pgw_kernel(const float* __restrict__ xht, const float* __restrict__ w,
+                                                             int64_t m, int k, const double* __restrict__ hht,
+                                                             double* __restrict__ part) {
+  extern __shared__ double sh[];  // hht (k x k), then per-warp sums
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) sh[e] = hht[e];
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    const float* wr = w + i * k;
+    const float* xr = xht + i * k;
+    for (int j = 0; j < k; ++j) {
+      double whh = 0.0;
+      for (int p = 0; p < k; ++p) whh = fma(double(wr[p]), sh[p * k + j], whh);
+      const double g = -2.0 * (double(xr[j]) - whh);
+      const double gi = wr[j] > 0.f ? g : fmin(0.0, g);
+      acc = fma(gi, gi, acc);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  double* ws = sh + k * k;
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < kPgwThreads / 32; ++q) s += ws[q];
+    part[blockIdx.x] = s;
+  }
+}
+
+template <int KW>
+void tc_resid_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* w_hi, const float* w_lo,
+                     const float* ht_hi, const float* ht_lo, double* part_obj, int grid, cudaStream_t stream) {
+  using C = RsCfg<KW>;
+  const int64_t npad = tc_st_pitch(n);
+  const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBM);
+  const CUtensorMap mwh = make_map_2d(w_hi, m, KW, KW, kBM);
+  const CUtensorMap mwl = make_map_2d(w_lo, m, KW, KW, kBM);
+  const CUtensorMap mhh = make_map_2d(ht_hi, npad, KW, KW, 32);
+  const CUtensorMap mhl = make_map_2d(ht_lo, npad, KW, KW, 32);
+  auto f = tc_resid_kernel<KW>;
+  RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
+  f<<<grid, kRsThreads, C::kSmem, stream>>>(mx, mwh, mwl, mhh, mhl, m, n, part_obj);
+  RNMF_CUDA_LAUNCH();
+}
+
+}  // namespace
+
+int launch_tc_prep_rows(const float* src, int c, int64_t n, float* st_hi, float* st_lo, cudaStream_t stream) {
+  const int npad = tc_npad(c);
+  const int64_t ld = tc_st_pitch(n);
+  const int blocks = int(std::min<int64_t>(ceil_div(int64_t(npad) * ld, 256), 148 * 8));
+  tc_prep_rows_kernel<<<blocks, 256, 0, stream>>>(src, c, n, npad, ld, st_hi, st_lo);
+  RNMF_CUDA_LAUNCH();
+  return 1;
+}
+
+int tc_resid_kw(int k) { return k <= 32 ? 32 : 64; }
+
+int launch_tc_resid_prep(const float* w, int64_t m, const float* h, int64_t n, int k, float* w_hi, float* w_lo,
+                         float* ht_hi, float* ht_lo, cudaStream_t stream) {
+  const int kw = tc_resid_kw(k);
+  const int64_t npad = tc_st_pitch(n);
+  const int64_t total = (m + npad) * kw;
+  const int blocks = int(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
+  tc_resid_prep_kernel<<<blocks, 256, 0, stream>>>(w, m, h, n, k, kw, npad, w_hi, w_lo, ht_hi, ht_lo);
+  RNMF_CUDA_LAUNCH();
+  return 1;
+}
+
+int tc_resid_blocks(int64_t m, int sm_count) { return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kBM), sm_count))); }
+
+int launch_tc_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const float* w_hi, const float* w_lo,
+                    const float* ht_hi, const float* ht_lo, int k, double* part_obj, int* nblocks, int sm_count,
+                    cudaStream_t stream) {
+  if ((ldx * sizeof(float)) % 16 != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0)
+    throw CudaError("tc_resid: X needs a 16-byte aligned base and row pitch");
+  if (k > 64) throw CudaError("tc_resid: k above 64");
+  const int grid = tc_resid_blocks(m, sm_count);
+  if (tc_resid_kw(k) == 32)
+    tc_resid_launch<32>(x, m, n, ldx, w_hi, w_lo, ht_hi, ht_lo, part_obj, grid, stream);
+  else
+    tc_resid_launch<64>(x, m, n, ldx, w_hi, w_lo, ht_hi, ht_lo, part_obj, grid, stream);
+  *nblocks = grid;
+  return 1;
+}
+
+int tc_pgw_blocks(int64_t m) { return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kPgwThreads), 148 * 4))); }
+
+int launch_tc_pgw(const float* xht, const float* w, int64_t m, int k, const double* hht, double* part_pgw,
+                  int* nblocks, cudaStream_t stream) {
+  const int blocks = tc_pgw_blocks(m);
+  const size_t smem = sizeof(double) * (size_t(k) * k + kPgwThreads / 32);
+  tc_pgw_kernel<<<blocks, kPgwThreads, smem, stream>>>(xht, w, m, k, hht, part_pgw);
+  RNMF_CUDA_LAUNCH();
+  *nblocks = blocks;
   return 1;
 }
 

@@ -5,6 +5,7 @@
 #include "../../include/rnmf_gpu.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_metrics.h"
 
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl.so.2 is opened at run time (row-sharded contexts)
@@ -320,6 +321,9 @@ template <typename T>
 class Engine {
  public:
   Engine(rnmf_gpu_context* ctx, Timer& tm) : ctx_(ctx), st_(ctx->stream), tm_(tm) {}
+  // arithmetic of the X passes (rnmf_solver_options.math_mode): TF32X3 also moves the full-space
+  // metrics onto the tensor cores (metrics_tc)
+  void set_math(int math_mode) { math_ = math_mode; }
 
   // ---- row sharding: this engine holds rows [row_off, row_off + m) of an m_total-row X --------
   bool sharded() const { return ctx_->shard.world > 0; }
@@ -556,6 +560,12 @@ class Engine {
   // writes [objective, pgrad_full] into res (device).
   // hht_in: H H^T (k x k, fp64) when the caller has it (the sweep kernel's V after every launch)
   void metrics(int k, const T* w, const T* h, double* res, const double* hht_in = nullptr) {
+    if constexpr (std::is_same<T, float>::value) {
+      if (math_ == RNMF_MATH_TF32X3 && k <= 64 && m_ > 0 && n_ > 0) {
+        metrics_tc(k, w, h, res, hht_in);
+        return;
+      }
+    }
     const T* x = x_;
     const int64_t m = m_, n = n_, ldx = ldx_;
     T* ht = ctx_->d<T>("met.ht", size_t(n) * k);
@@ -635,9 +645,79 @@ class Engine {
     metrics_passes_ += x_passes_;
   }
 
+  // Full-space metrics on the tensor cores (math_mode TF32X3, fp32): three X passes, each a
+  // tcgen05 3xTF32 kernel with fp32-promoted accumulation (tc_metrics.h):
+  //   X H^T -> projected grad_W, X^T W -> projected grad_H, explicit residual -> objective.
+  void metrics_tc(int k, const float* w, const float* h, double* res, const double* hht_in) {
+    const float* x = reinterpret_cast<const float*>(x_);
+    const int64_t m = m_, n = n_, ldx = ldx_;
+    const int sms = ctx_->sm_count;
+    double* hht = ctx_->d<double>("met.hht", size_t(k) * k);
+    double* wtw = ctx_->d<double>("met.wtw", size_t(k) * k);
+    double* gpart = ctx_->d<double>("met.gpart", size_t(gram_parts(std::max(m, n))) * k * k);
+    double* gpart2 = ctx_->d<double>("met.gpart2", size_t(gram_parts(std::max(m, n))) * k * k);
+    const int npad = tc_npad(k), kw = tc_resid_kw(k);
+    float* sth = ctx_->d<float>("tcm.sth", size_t(npad) * size_t(tc_st_pitch(n)));
+    float* stl = ctx_->d<float>("tcm.stl", size_t(npad) * size_t(tc_st_pitch(n)));
+    float* swh = ctx_->d<float>("tcm.swh", size_t(npad) * size_t(tc_st_pitch(m)));
+    float* swl = ctx_->d<float>("tcm.swl", size_t(npad) * size_t(tc_st_pitch(m)));
+    float* wh = ctx_->d<float>("tcm.wh", size_t(m) * kw);
+    float* wl = ctx_->d<float>("tcm.wl", size_t(m) * kw);
+    float* hth = ctx_->d<float>("tcm.hth", size_t(tc_st_pitch(n)) * kw);
+    float* htl = ctx_->d<float>("tcm.htl", size_t(tc_st_pitch(n)) * kw);
+    float* xht = ctx_->d<float>("tcm.xht", size_t(m) * k);
+    const int splits = tc_xtw_splits(m, n, sms);
+    float* part = ctx_->d<float>("tcm.part", size_t(splits) * n * k);
+    double* pobj = ctx_->d<double>("tcm.pobj", size_t(tc_resid_blocks(m, sms)));
+    double* ppgw = ctx_->d<double>("tcm.ppgw", size_t(tc_pgw_blocks(m)));
+    double* ppgh = ctx_->d<double>("tcm.ppgh", size_t(grad_h_blocks(n, k)));
+    double* tmp = ctx_->d<double>("met.tmp", 4);
+    tm_.span(kMetrics, [&] {
+      if (hht_in)
+        hht = const_cast<double*>(hht_in);
+      else
+        tm_.launches += launch_gram_cols<float>(h, k, n, gpart, hht, st_);
+      tm_.launches += launch_gram_rows<float>(w, m, k, gpart2, wtw, st_);
+      allreduce(wtw, size_t(k) * k);  // W^T W over all rows (H H^T is replicated)
+      // X H^T (m x k) -> projected grad_W partials
+      int b1 = 0, b2 = 0, b0 = 0;
+      tm_.launches += launch_tc_prep_rows(h, k, n, sth, stl, st_);
+      tm_.launches += launch_tc_xw(x, m, n, ldx, sth, stl, k, xht, true, sms, st_);
+      tm_.launches += launch_tc_pgw(xht, w, m, k, hht, ppgw, &b1, st_);
+      // X^T W (n x k split partials) -> projected grad_H partials
+      tm_.launches += launch_tc_prep_st(w, m, k, swh, swl, st_);
+      tm_.launches += launch_tc_xtw(x, m, n, ldx, swh, swl, k, part, splits, true, sms, st_);
+      if (sharded()) {
+        float* wtx1 = ctx_->d<float>("met.wtx1", size_t(n) * k);
+        tm_.launches += launch_splitk_reduce<float>(part, splits, n, k, wtx1, false, st_);
+        allreduce(wtx1, size_t(n) * k);
+        tm_.launches += launch_grad_h_reduce<float>(wtx1, 1, n, k, h, wtw, ppgh, &b2, st_);
+      } else {
+        tm_.launches += launch_grad_h_reduce<float>(part, splits, n, k, h, wtw, ppgh, &b2, st_);
+      }
+      // objective from the explicit residual
+      tm_.launches += launch_tc_resid_prep(w, m, h, n, k, wh, wl, hth, htl, st_);
+      tm_.launches += launch_tc_resid(x, m, n, ldx, wh, wl, hth, htl, k, pobj, &b0, sms, st_);
+      if (!sharded()) {
+        tm_.launches += launch_metrics_finalize(pobj, b0, ppgw, b1, ppgh, b2, res, st_);
+      } else {
+        tm_.launches += launch_sum_parts(pobj, b0, res, st_);
+        tm_.launches += launch_sum_parts(ppgw, b1, tmp, st_);
+        allreduce(res, 1);
+        allreduce(tmp, 1);
+        tm_.launches += launch_sum_parts(ppgh, b2, tmp + 1, st_);
+        tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
+      }
+    });
+    x_passes_ = 3;
+    metrics_bytes_ += 3.0 * double(m) * double(n) * sizeof(float);
+    metrics_passes_ += 3;
+  }
+
   double sum() const { return sum_; }
   double sumsq() const { return sumsq_; }
   double sketch_bytes_ = 0, metrics_bytes_ = 0;
+  int math_ = RNMF_MATH_EXACT;
   int64_t qr_calls_ = 0, qr_fallbacks_ = 0;
   int64_t sketch_passes_ = 0, metrics_passes_ = 0;
 
@@ -990,6 +1070,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   ctx->last = rnmf_stage_times{};
   Timer tm(ctx);
   Engine<T> eng(ctx, tm);
+  eng.set_math(o.math_mode);
   if (m < 0 || n < 0) throw ShapeError("X has negative dimensions " + shape_string(m, n));
   const int64_t mt = m_total < 0 ? m : m_total;
   eng.set_rows(row_off, mt);
@@ -1249,6 +1330,7 @@ static void fit_compressed_impl(rnmf_gpu_context* ctx, const void* x_in, int loc
   ctx->last = rnmf_stage_times{};
   Timer tm(ctx);
   Engine<T> eng(ctx, tm);
+  eng.set_math(o.math_mode);
   const T* x = nullptr;
   if (m * n > 0) {
     x = eng.import_x(x_in, location, m, n);

@@ -131,7 +131,7 @@ int main(int argc, char** argv) {
     report("ffma_tma", ms);
     launch_tc_prep_st(ds, n, c, dh, dl, 0);
     for (int x3 = 1; x3 >= 0; --x3)
-      for (int ch : {100000, 4, 2, 1}) {
+      for (int ch : {16, 8, 4}) {
         if (!x3 && ch != 2) continue;
         tc_set_chunk(ch);
         ms = timeit([&] { launch_tc_xw(dx, m, n, ldx, dh, dl, c, dy, x3, sms, 0); });
@@ -161,7 +161,7 @@ int main(int argc, char** argv) {
     launch_tc_prep_st(dq, m, c, dh, dl, 0);
     const int tsp = tc_xtw_splits(m, n, sms);
     for (int x3 = 1; x3 >= 0; --x3)
-      for (int ch : {100000, 4, 2, 1}) {
+      for (int ch : {16, 8, 4}) {
         if (!x3 && ch != 2) continue;
         tc_set_chunk(ch);
         ms = timeit([&] {
