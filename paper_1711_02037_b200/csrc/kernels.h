@@ -178,14 +178,21 @@ enum SweepFlags : int {
   kReseed = 256,      // reseed_dead: liveness stamps per sweep, stop at a dead component (host reseeds)
   kEvalPrev = 512,    // evaluate + record sweep t_begin - 1 first (after a host-side reseed)
 };
-// Sync block of the sweep kernel (zeroed before every launch): the grid-barrier counter at byte 0,
-// then a 3-slot ring of 64-bit fixed-point accumulators for the column step.
+// Sync block of the sweep kernel (zeroed before every launch): the legacy grid-barrier counter at
+// byte 0 (cross-GPU counter at byte 64), a 3-slot ring of 64-bit fixed-point accumulators for the
+// column step, then the replicated grid-barrier counters.  Both the accumulators and the barrier
+// counter are replicated on separate 128-byte L2 lines (CTA g uses replica g % reps; readers sum
+// the replicas -- integer sums, so the result is exact and order-free): the 148 same-address
+// atomics of one column step become 148 / reps per line.
 constexpr int kColAccMax = 136;      // entries per slot, >= l + 1
 constexpr int kColAccSpacing = 16;   // words between entries: one 128-byte L2 line per entry (the
                                      // atomics of different entries do not serialise on a line)
-constexpr int kColAccStride = kColAccMax * kColAccSpacing;
-// zeroed part: local barrier counter (byte 0), cross-GPU barrier counter (byte 64), accumulators
-constexpr size_t kSweepSyncBytes = 128 + 3 * size_t(kColAccStride) * sizeof(unsigned long long);
+constexpr int kColAccReps = 4;       // accumulator replicas per entry
+constexpr int kColAccStride = kColAccReps * kColAccMax * kColAccSpacing;  // words per slot
+constexpr int kBarReps = 8;          // grid-barrier counter replicas (one 128-byte line each)
+constexpr size_t kSweepBarOffset = 128 + 3 * size_t(kColAccStride) * sizeof(unsigned long long);
+// zeroed part: counters (bytes 0 / 64), accumulators, replicated barrier counters
+constexpr size_t kSweepSyncBytes = kSweepBarOffset + size_t(kBarReps) * 128;
 // Row-sharded runs (one process per GPU): after the zeroed part, a 2-slot exchange buffer of
 // kMaxWorld x kXMax doubles per slot that peers write into (never needs clearing).
 constexpr int kMaxWorld = 8;

@@ -263,7 +263,23 @@ struct Sweeper {
   __device__ __forceinline__ double* fin_base() { return a.fin + int64_t(slot) * fin_slot_len; }
   __device__ __forceinline__ void next_slot() { slot ^= 1; }
 
-  __device__ void barrier() { grid_barrier(a.barrier, epoch); }
+  // Grid barrier over kBarReps replicated counters: CTA g arrives (release) on counter g % reps,
+  // lanes 0..reps-1 of warp 0 poll one counter each (acquire) until their sum reaches the target.
+  __device__ void barrier() {
+    __syncthreads();
+    epoch += 1;
+    if (tid < 32) {
+      unsigned* ctr = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(a.barrier) + kSweepBarOffset);
+      constexpr int kLine = 128 / int(sizeof(unsigned));
+      if (tid == 0) red_release_gpu_add(ctr + (g % kBarReps) * kLine, 1u);
+      const unsigned target = epoch * unsigned(G);
+      while (true) {
+        const unsigned v = tid < kBarReps ? ld_acquire_gpu(ctr + tid * kLine) : 0u;
+        if (__reduce_add_sync(0xffffffffu, v) >= target) break;
+      }
+    }
+    __syncthreads();
+  }
 
   // ---- row sharding across GPUs (a.world >= 1; one process per GPU, peers mapped by IPC) ------
   __device__ __forceinline__ bool sharded() const { return a.world > 0; }
@@ -417,7 +433,8 @@ struct Sweeper {
       allreduce1(L1, wr);
       return;
     }
-    const int64_t off = (cstep % 3) * kColAccStride + tid * kColAccSpacing;
+    const int64_t slot0 = (cstep % 3) * kColAccStride;
+    const int64_t off = slot0 + (int64_t(g % kColAccReps) * kColAccMax + tid) * kColAccSpacing;
     unsigned long long* cur = colacc + off;
     if (tid < L1) {
       const long long fx = __double2ll_rn(v * sc[tid < l ? 0 : 1]);  // exact power-of-two scaling
@@ -431,7 +448,10 @@ struct Sweeper {
         atomicAdd(cur, static_cast<unsigned long long>(fx));
       }
     }
-    if (g == 0 && tid < L1) colacc[((cstep + 1) % 3) * kColAccStride + tid * kColAccSpacing] = 0ull;
+    if (g == 0 && tid < L1)
+#pragma unroll
+      for (int rp = 0; rp < kColAccReps; ++rp)
+        colacc[((cstep + 1) % 3) * kColAccStride + (int64_t(rp) * kColAccMax + tid) * kColAccSpacing] = 0ull;
     prof_tick(kPfOther);
     if (sharded())
       xbarrier();
@@ -439,7 +459,11 @@ struct Sweeper {
       barrier();
     prof_tick(kPfBarrier1);
     if (tid < L1) {
-      const long long sum = static_cast<long long>(ld_cg(cur));
+      unsigned long long acc = 0ull;
+#pragma unroll
+      for (int rp = 0; rp < kColAccReps; ++rp)
+        acc += ld_cg(colacc + slot0 + (int64_t(rp) * kColAccMax + tid) * kColAccSpacing);
+      const long long sum = static_cast<long long>(acc);
       wr(tid, double(sum) * inv[tid < l ? 0 : 1]);
     }
     ++cstep;
@@ -718,10 +742,37 @@ struct Sweeper {
       // rows of the warp (lane L ends with entry L of each 32-entry chunk), then cross-warp in order
 #pragma unroll
       for (int chunk = 0; chunk < (LREG + 31) / 32; ++chunk) {
-        if (chunk * 32 < L1) {
-          auto val = [&](int i) -> double {  // entry i of this thread's contribution vector
-            return (i < l) ? qrow[i < LREG ? i : 0] * wd : (i == l ? wd * wd : 0.0);
-          };
+        auto val = [&](int i) -> double {  // entry i of this thread's contribution vector
+          return (i < l) ? qrow[i < LREG ? i : 0] * wd : (i == l ? wd * wd : 0.0);
+        };
+        if (chunk > 0 && chunk * 32 < L1 && L1 - chunk * 32 <= 8) {
+          // short tail chunk (<= 8 live entries, e.g. l = 36): 3-stage reduce-scatter of 8 values,
+          // then a 2-stage all-reduce within lane quads -- 9 shuffles instead of 31
+          double v[4];
+          {
+            const bool hi = (lane & 16) != 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int ia = chunk * 32 + e, ib = ia + 4;
+              const double va = (ia < LREG || ia == l) ? val(ia) : 0.0;
+              const double vb = (ib < LREG || ib == l) ? val(ib) : 0.0;
+              v[e] = (hi ? vb : va) + __shfl_xor_sync(0xffffffffu, hi ? va : vb, 16);
+            }
+          }
+          {
+            const bool hi = (lane & 8) != 0;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) v[e] = (hi ? v[e + 2] : v[e]) + __shfl_xor_sync(0xffffffffu, hi ? v[e] : v[e + 2], 8);
+          }
+          {
+            const bool hi = (lane & 4) != 0;
+            v[0] = (hi ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, hi ? v[0] : v[1], 4);
+          }
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+          const int i = chunk * 32 + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+          if ((lane & 3) == 0 && i < L1) red[wid * kRedStride + i] = v[0];
+        } else if (chunk * 32 < L1) {
           double v[16];
           {
             const bool hi = (lane & 16) != 0;

@@ -317,6 +317,7 @@ constexpr ncclDataType_t nccl_type() {
   else return ncclInt64;
 }
 
+
 template <typename T>
 class Engine {
  public:
