@@ -1352,7 +1352,53 @@ struct Sweeper {
           }
         }
       }
-    } else
+    } else {
+    bool done = false;
+    if constexpr (QS && LREG > 0) {
+      // register-resident Q rows: E packed (even row stride, zero pad) into the red scratch so each
+      // i step is 16-byte broadcast loads + DFMAs against the row already in registers
+      const int kE = (k + 1) & ~1;
+      if (l * kE <= kRedLen) {
+        __syncthreads();
+        for (int e = tid; e < l * kE; e += kSwThreads) {
+          const int i = e / kE, j = e % kE;
+          red[e] = j < k ? Em[i * kp + j] : 0.0;
+        }
+        __syncthreads();
+        if (tid < R) {
+          for (int j0 = 0; j0 < k; j0 += 8) {
+            double sacc[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) sacc[t] = 0.0;
+#pragma unroll
+            for (int i = 0; i < LREG; ++i) {
+              if (i < l) {
+                const double2* ep = reinterpret_cast<const double2*>(red + i * kE + j0);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if (j0 + 2 * u < k) {
+                    const double2 ev = ep[u];
+                    sacc[2 * u] += qrow[i] * ev.x;
+                    sacc[2 * u + 1] += qrow[i] * ev.y;
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (j0 + t < k) {
+                const double gv = -2.0 * sacc[t];
+                const double gp = w_get(tid, j0 + t) > T(0) ? gv : fmin(0.0, gv);
+                acc += gp * gp;
+              }
+            }
+          }
+        }
+        __syncthreads();  // red is block_sum's scratch next
+        done = true;
+      }
+    }
+    if (!done)
     for (int64_t r = tid; r < R; r += kSwThreads) {
       for (int j0 = 0; j0 < k; j0 += 16) {
         double sacc[16];
@@ -1374,6 +1420,7 @@ struct Sweeper {
           }
         }
       }
+    }
     }
     const double tot = block_sum(acc);
     if (tid == 0) part_base()[g] = tot;
