@@ -1010,4 +1010,298 @@ int launch_tc_pgw(const float* xht, const float* w, int64_t m, int k, const doub
   return 1;
 }
 
+
+// ================================================================================================
+// Fused metrics pass for k <= 32 (tc_metrics.h launch_tc_xht_resid): ONE read of X gives both
+//   X H^T (3xTF32, as tc_xw_kernel with S^T = H)   and   sum (X - W H)^2 (as tc_resid_kernel)
+// per 128-row tile.  Ring stage = [X 16 KB][H slab hi | lo (NPAD rows each)][H^T slab hi | lo (32
+// rows each)]; the W tile (hi, lo; one 32-wide K atom) is resident per tile; the lo X tiles use
+// the split warps' ring.  TMEM: X H^T accumulator chunks (2 x 2 NPAD columns) and a 4-deep ring
+// of 64-column W H buffers.  Epilogue warps: per stage the residual of their row (X row from the
+// swizzled stage), per chunk the X H^T drain into fp32 registers.
+namespace {
+
+template <int NPAD>
+struct FzCfg {
+  static constexpr int kSBytes = NPAD * kBK * 4;
+  static constexpr int kHtBytes = 2 * 32 * 128;                       // H^T hi | lo (32 rows each)
+  static constexpr int kWBytes = 2 * kXTileBytes;                     // W hi, lo (128 rows x 32)
+  static constexpr int kStageBytes = kXTileBytes + 2 * kSBytes + kHtBytes;
+  static constexpr int kLoBytes = kLoSlots * kXTileBytes;
+  static constexpr int kStages = std::min(8, (kSmemBudget - kWBytes - kLoBytes - 2048) / kStageBytes);
+  static constexpr int kAccCols = 2 * NPAD;
+  static constexpr int kRsBase = 2 * kAccCols;                        // W H ring after the X H^T buffers
+  static constexpr int kTmemCols = 512;
+  static constexpr size_t kSmem = size_t(kWBytes) + size_t(kStages) * kStageBytes + kLoBytes + 1024 + 512;
+  static_assert(kStages >= 2, "ring too shallow");
+  static_assert(kRsBase + kRsTmemBufs * 64 <= 512, "TMEM");
+};
+
+struct FzParams {
+  int64_t m, n;
+  int c;
+  float* y;          // X H^T (m x c)
+  int chunk;
+  double* part_obj;  // per-CTA residual partials
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
+    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmShi,
+    const __grid_constant__ CUtensorMap tmSlo, const __grid_constant__ CUtensorMap tmWhi,
+    const __grid_constant__ CUtensorMap tmWlo, const __grid_constant__ CUtensorMap tmHhi,
+    const __grid_constant__ CUtensorMap tmHlo, FzParams p) {
+  using C = FzCfg<NPAD>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* wsm = base;
+  auto xst = [&](int s) { return base + C::kWBytes + size_t(s) * C::kStageBytes; };
+  auto shi = [&](int s) { return xst(s) + kXTileBytes; };
+  auto htp = [&](int s) { return shi(s) + 2 * C::kSBytes; };
+  auto lo = [&](int j) { return base + C::kWBytes + size_t(S) * C::kStageBytes + size_t(j) * kXTileBytes; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::kWBytes + size_t(S) * C::kStageBytes + C::kLoBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + S;
+  uint64_t* lofull = empty + S;
+  uint64_t* loempty = lofull + kLoSlots;
+  uint64_t* tfull = loempty + kLoSlots;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + kRsTmemBufs;
+  uint64_t* wfull = rempty + kRsTmemBufs;
+  uint64_t* wempty = wfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+  double* red = reinterpret_cast<double*>(wempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = ceil_div(p.m, kBM);
+  const int nk = int(ceil_div(p.n, kBK));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1 + 4);
+    }
+    for (int j = 0; j < kLoSlots; ++j) {
+      tc::mbar_init(&lofull[j], kSplitThreads);
+      tc::mbar_init(&loempty[j], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 128);
+    }
+    for (int b = 0; b < kRsTmemBufs; ++b) {
+      tc::mbar_init(&rfull[b], 1);
+      tc::mbar_init(&rempty[b], 128);
+    }
+    tc::mbar_init(wfull, 1);
+    tc::mbar_init(wempty, 1);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmShi);
+    tc::tma_prefetch(&tmSlo);
+    tc::tma_prefetch(&tmWhi);
+    tc::tma_prefetch(&tmWlo);
+    tc::tma_prefetch(&tmHhi);
+    tc::tma_prefetch(&tmHlo);
+  }
+  if (warp == 1) tc::tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      uint32_t it = 0, ti = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+        tc::mbar_wait(wempty, (ti & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(wfull, uint32_t(C::kWBytes));
+        tc::tma_load_2d(wsm, &tmWhi, wfull, 0, int(t * kBM));
+        tc::tma_load_2d(wsm + kXTileBytes, &tmWlo, wfull, 0, int(t * kBM));
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = int(it % S);
+          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
+          tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
+          tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
+          tc::tma_load_2d(shi(s) + C::kSBytes, &tmSlo, &full[s], kc * kBK, 0);
+          tc::tma_load_2d(htp(s), &tmHhi, &full[s], 0, kc * kBK);
+          tc::tma_load_2d(htp(s) + 4096, &tmHlo, &full[s], 0, kc * kBK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc32 = tc::make_idesc_tf32(32, false, false);
+    constexpr uint32_t idesc64 = tc::make_idesc_tf32(64, false, false);
+    auto adesc = [](uint32_t b, int k) { return tc::make_sdesc(b + k * 32, 16, 1024); };
+    uint32_t it = 0, ci = 0, ti = 0;
+    uint32_t d = tmem_base;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+      tc::mbar_wait(wfull, ti & 1);
+      tc::tc_fence_after();
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int kin = kc % p.chunk;
+        const bool cend = (kin == p.chunk - 1) || (kc == nk - 1);
+        const int acc = int(ci & 1);
+        if (kin == 0) {
+          tc::mbar_wait(&tempty[acc], ((ci >> 1) & 1) ^ 1);
+          d = tmem_base + uint32_t(acc * C::kAccCols);
+        }
+        const int s = int(it % S), j = int(it % kLoSlots), b = int(it % kRsTmemBufs);
+        tc::mbar_wait(&rempty[b], ((it / kRsTmemBufs) & 1) ^ 1);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&lofull[j], (it / kLoSlots) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          // X H^T chunk: X_hi [H_hi; H_lo]^T, += X_lo H_hi^T
+          issue_stage<NPAD, true, false>(d, tc::smem_u32(xst(s)), tc::smem_u32(lo(j)), tc::smem_u32(shi(s)), kin == 0,
+                                         adesc);
+          // W H (this stage's 32 columns): [W_hi H_hi | W_hi H_lo], += W_lo H_hi
+          const uint32_t dr = tmem_base + uint32_t(C::kRsBase + b * 64);
+          const uint32_t wa = tc::smem_u32(wsm), ha = tc::smem_u32(htp(s));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t whi = tc::make_sdesc(wa + kk * 32, 16, 1024);
+            const uint64_t wlo = tc::make_sdesc(wa + kXTileBytes + kk * 32, 16, 1024);
+            const uint64_t hb = tc::make_sdesc(ha + kk * 32, 16, 1024);
+            tc::umma_tf32(dr, whi, hb, idesc64, kk != 0);
+            tc::umma_tf32(dr + 32, wlo, hb, idesc32, 1u);
+          }
+          tc::umma_commit(&empty[s]);
+          tc::umma_commit(&loempty[j]);
+          tc::umma_commit(&rfull[b]);
+          if (cend) tc::umma_commit(&tfull[acc]);
+          if (kc == nk - 1) tc::umma_commit(wempty);
+        }
+        if (cend) ++ci;
+        __syncwarp();
+      }
+    }
+  } else if (warp < 4 || warp >= 8) {
+    const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = int(it % S), j = int(it % kLoSlots);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&loempty[j], ((it / kLoSlots) & 1) ^ 1);
+        split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(xst(s)), reinterpret_cast<float4*>(lo(j)), st);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&lofull[j]);
+      }
+    }
+  } else {
+    const int sub = warp & 3;
+    const int r = sub * 32 + lane;
+    const uint32_t lane_off = uint32_t(sub * 32) << 16;
+    double racc = 0.0;
+    uint32_t it = 0, ci = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t row = t * kBM + r;
+      float a[NPAD];
+#pragma unroll
+      for (int q = 0; q < NPAD; ++q) a[q] = 0.f;
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = int(it % S), b = int(it % kRsTmemBufs);
+        // residual of this stage's 32 columns
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&rfull[b], (it / kRsTmemBufs) & 1);
+        tc::tc_fence_after();
+        uint32_t d0[32], d1[32];
+        const uint32_t taddr = tmem_base + lane_off + uint32_t(C::kRsBase + b * 64);
+        tc::tmem_ld_32x32b_x32(taddr, d0);
+        tc::tmem_ld_32x32b_x32(taddr + 32, d1);
+        const uint32_t xrow = tc::smem_u32(xst(s)) + uint32_t(r) * 128u;
+        float xv[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t v0, v1, v2, v3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)));
+          xv[4 * c] = __uint_as_float(v0), xv[4 * c + 1] = __uint_as_float(v1);
+          xv[4 * c + 2] = __uint_as_float(v2), xv[4 * c + 3] = __uint_as_float(v3);
+        }
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&rempty[b]);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        float ss = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float e = xv[c] - (__uint_as_float(d0[c]) + __uint_as_float(d1[c]));
+          ss = fmaf(e, e, ss);
+        }
+        racc += double(ss);
+        // X H^T chunk drain
+        const bool cend = (kc % p.chunk == p.chunk - 1) || (kc == nk - 1);
+        if (cend) {
+          const int acc = int(ci & 1);
+          tc::mbar_wait(&tfull[acc], (ci >> 1) & 1);
+          tc::tc_fence_after();
+          drain_acc<NPAD, true>(tmem_base + lane_off + uint32_t(acc * C::kAccCols), a);
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[acc]);
+          ++ci;
+        }
+      }
+      if (row < p.m) {
+#pragma unroll
+        for (int q = 0; q < NPAD; ++q)
+          if (q < p.c) p.y[row * p.c + q] = a[q];
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
+    if (lane == 0) red[sub] = racc;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) p.part_obj[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+template <int NPAD>
+void tc_xht_resid_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
+                         const float* w_hi, const float* w_lo, const float* ht_hi, const float* ht_lo, int k,
+                         float* xht, double* part_obj, int grid, cudaStream_t stream) {
+  using C = FzCfg<NPAD>;
+  const int64_t ldst = tc_st_pitch(n);
+  const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBM);
+  const CUtensorMap mh = make_map_2d(st_hi, NPAD, n, ldst, NPAD);
+  const CUtensorMap ml = make_map_2d(st_lo, NPAD, n, ldst, NPAD);
+  const CUtensorMap mwh = make_map_2d(w_hi, m, 32, 32, kBM);
+  const CUtensorMap mwl = make_map_2d(w_lo, m, 32, 32, kBM);
+  const CUtensorMap mhh = make_map_2d(ht_hi, ldst, 32, 32, 32);
+  const CUtensorMap mhl = make_map_2d(ht_lo, ldst, 32, 32, 32);
+  FzParams p{m, n, k, xht, tc_chunk_stages(), part_obj};
+  auto f = tc_xht_resid_kernel<NPAD>;
+  RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
+  f<<<grid, kTcThreadsX3, C::kSmem, stream>>>(mx, mh, ml, mwh, mwl, mhh, mhl, p);
+  RNMF_CUDA_LAUNCH();
+}
+
+}  // namespace
+
+int launch_tc_xht_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
+                        const float* w_hi, const float* w_lo, const float* ht_hi, const float* ht_lo, int k, float* xht,
+                        double* part_obj, int* nblocks, int sm_count, cudaStream_t stream) {
+  if ((ldx * sizeof(float)) % 16 != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0)
+    throw CudaError("tc_xht_resid: X needs a 16-byte aligned base and row pitch");
+  if (k > 32 || tc_resid_kw(k) != 32) throw CudaError("tc_xht_resid: k above 32");
+  const int grid = tc_resid_blocks(m, sm_count);
+  if (tc_npad(k) == 16)
+    tc_xht_resid_launch<16>(x, m, n, ldx, st_hi, st_lo, w_hi, w_lo, ht_hi, ht_lo, k, xht, part_obj, grid, stream);
+  else
+    tc_xht_resid_launch<32>(x, m, n, ldx, st_hi, st_lo, w_hi, w_lo, ht_hi, ht_lo, k, xht, part_obj, grid, stream);
+  *nblocks = grid;
+  return 1;
+}
+
 }  // namespace rnmf_gpu

@@ -646,9 +646,10 @@ class Engine {
     metrics_passes_ += x_passes_;
   }
 
-  // Full-space metrics on the tensor cores (math_mode TF32X3, fp32): three X passes, each a
-  // tcgen05 3xTF32 kernel with fp32-promoted accumulation (tc_metrics.h):
-  //   X H^T -> projected grad_W, X^T W -> projected grad_H, explicit residual -> objective.
+  // Full-space metrics on the tensor cores (math_mode TF32X3, fp32): tcgen05 3xTF32 kernels with
+  // fp32-promoted accumulation (tc_metrics.h):
+  //   X H^T -> projected grad_W, X^T W -> projected grad_H, explicit residual -> objective;
+  // for k <= 32 the X H^T and residual kernels are one (two X passes per evaluation, else three).
   void metrics_tc(int k, const float* w, const float* h, double* res, const double* hht_in) {
     const float* x = reinterpret_cast<const float*>(x_);
     const int64_t m = m_, n = n_, ldx = ldx_;
@@ -673,6 +674,7 @@ class Engine {
     double* ppgw = ctx_->d<double>("tcm.ppgw", size_t(tc_pgw_blocks(m)));
     double* ppgh = ctx_->d<double>("tcm.ppgh", size_t(grad_h_blocks(n, k)));
     double* tmp = ctx_->d<double>("met.tmp", 4);
+    const bool fused = k <= 32 && !std::getenv("RNMF_NO_FUSED_RESID");
     tm_.span(kMetrics, [&] {
       if (hht_in)
         hht = const_cast<double*>(hht_in);
@@ -683,7 +685,13 @@ class Engine {
       // X H^T (m x k) -> projected grad_W partials
       int b1 = 0, b2 = 0, b0 = 0;
       tm_.launches += launch_tc_prep_rows(h, k, n, sth, stl, st_);
-      tm_.launches += launch_tc_xw(x, m, n, ldx, sth, stl, k, xht, true, sms, st_);
+      tm_.launches += launch_tc_resid_prep(w, m, h, n, k, wh, wl, hth, htl, st_);
+      if (fused) {  // X H^T and the residual in one X pass
+        tm_.launches += launch_tc_xht_resid(x, m, n, ldx, sth, stl, wh, wl, hth, htl, k, xht, pobj, &b0, sms, st_);
+      } else {
+        tm_.launches += launch_tc_xw(x, m, n, ldx, sth, stl, k, xht, true, sms, st_);
+        tm_.launches += launch_tc_resid(x, m, n, ldx, wh, wl, hth, htl, k, pobj, &b0, sms, st_);
+      }
       tm_.launches += launch_tc_pgw(xht, w, m, k, hht, ppgw, &b1, st_);
       // X^T W (n x k split partials) -> projected grad_H partials
       tm_.launches += launch_tc_prep_st(w, m, k, swh, swl, st_);
@@ -696,9 +704,6 @@ class Engine {
       } else {
         tm_.launches += launch_grad_h_reduce<float>(part, splits, n, k, h, wtw, ppgh, &b2, st_);
       }
-      // objective from the explicit residual
-      tm_.launches += launch_tc_resid_prep(w, m, h, n, k, wh, wl, hth, htl, st_);
-      tm_.launches += launch_tc_resid(x, m, n, ldx, wh, wl, hth, htl, k, pobj, &b0, sms, st_);
       if (!sharded()) {
         tm_.launches += launch_metrics_finalize(pobj, b0, ppgw, b1, ppgh, b2, res, st_);
       } else {
@@ -710,9 +715,9 @@ class Engine {
         tm_.launches += launch_sum_parts(tmp, 2, res + 1, st_);
       }
     });
-    x_passes_ = 3;
-    metrics_bytes_ += 3.0 * double(m) * double(n) * sizeof(float);
-    metrics_passes_ += 3;
+    x_passes_ = fused ? 2 : 3;
+    metrics_bytes_ += double(x_passes_) * double(m) * double(n) * sizeof(float);
+    metrics_passes_ += x_passes_;
   }
 
   double sum() const { return sum_; }

@@ -29,6 +29,12 @@ int tc_resid_blocks(int64_t m, int sm_count);
 
 // part_pgw[b] = partial sums of the projected grad_W^2, grad_W = -2 (XH^T - W (H H^T)) (fp64 math
 // on the fp32 X H^T, W and the fp64 H H^T); returns the number of partials via *nblocks
+// k <= 32: X H^T and the residual partials in ONE X pass (operands as for launch_tc_xw with
+// S^T = H via launch_tc_prep_rows, and launch_tc_resid_prep); part_obj holds tc_resid_blocks(m)
+int launch_tc_xht_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
+                        const float* w_hi, const float* w_lo, const float* ht_hi, const float* ht_lo, int k, float* xht,
+                        double* part_obj, int* nblocks, int sm_count, cudaStream_t stream);
+
 int launch_tc_pgw(const float* xht, const float* w, int64_t m, int k, const double* hht, double* part_pgw,
                   int* nblocks, cudaStream_t stream);
 int tc_pgw_blocks(int64_t m);
