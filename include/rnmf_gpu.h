@@ -11,6 +11,8 @@
  *   rnmf_gpu_rhals_update_W       <- rnmf::rhals_update_W       p/include/rnmf/rhals.hpp:33, p/src/rhals.cpp:107-114
  *   rnmf_gpu_rhals_update_H       <- rnmf::rhals_update_H       p/include/rnmf/rhals.hpp:27, p/src/rhals.cpp:116-119
  *   rnmf_gpu_rqb                  <- rnmf::rqb                  p/include/rnmf/sketch.hpp:64, p/src/sketch.cpp:52-71
+ *   rnmf_gpu_rqb_streaming        <- rnmf::rqb_streaming        p/include/rnmf/sketch.hpp:71, p/src/sketch.cpp:73-116
+ *   rnmf_gpu_rqb_streaming_file   <- rqb_streaming(FileColumnSource) p/include/rnmf/data_io.hpp:32-45
  *
  * Types mirror the reference field for field:
  *   rnmf_reg_config      <- RegConfig      p/include/rnmf/hals.hpp:15-20
@@ -208,6 +210,31 @@ int rnmf_gpu_rqb(rnmf_gpu_context* ctx, const void* a, int dtype, int location, 
                  int64_t n, int64_t target_rank, int64_t oversampling, int64_t power_iterations,
                  int test_matrix, uint64_t seed, const double* omega, int math_mode,
                  void* q_out, void* b_out, int64_t* l_out, char* err, size_t err_cap);
+
+/* ColumnSource::read_columns (p/include/rnmf/sketch.hpp:26-33): write columns [first, first +
+ * count) of the m x n source into dst as an m x count row-major double block; return 0 on
+ * success, nonzero on failure (reported as RNMF_IO_ERROR). */
+typedef int (*rnmf_column_reader)(void* user, int64_t first, int64_t count, double* dst);
+
+/* rqb_streaming(src, SketchOptions{..., block_size, ...}) -> {Q m x l, B l x n}, fp64
+ * (p/include/rnmf/sketch.hpp:71, p/src/sketch.cpp:73-116).  The source is read in column blocks
+ * of block_size, 2 + power_iterations passes; Omega from Rng(seed) (or the n x l `omega`
+ * override).  q_out (m x l) / b_out (l x n) are host row-major doubles; both NULL: only *l_out. */
+int rnmf_gpu_rqb_streaming(rnmf_gpu_context* ctx, rnmf_column_reader reader, void* user, int64_t m,
+                           int64_t n, int64_t target_rank, int64_t oversampling,
+                           int64_t power_iterations, int test_matrix, int64_t block_size,
+                           uint64_t seed, const double* omega, double* q_out, double* b_out,
+                           int64_t* l_out, char* err, size_t err_cap);
+
+/* rqb_streaming over FileColumnSource(path) (p/include/rnmf/data_io.hpp:32-45,
+ * p/src/data_io.cpp:185-223): the RNMFMAT1 binary format (8-byte magic, rows and cols as
+ * little-endian u64, row-major float64 payload).  *m_out / *n_out receive the file's shape; call
+ * with q_out = b_out = NULL first to size the outputs. */
+int rnmf_gpu_rqb_streaming_file(rnmf_gpu_context* ctx, const char* path, int64_t target_rank,
+                                int64_t oversampling, int64_t power_iterations, int test_matrix,
+                                int64_t block_size, uint64_t seed, const double* omega,
+                                double* q_out, double* b_out, int64_t* m_out, int64_t* n_out,
+                                int64_t* l_out, char* err, size_t err_cap);
 
 /* rhals_update_W(cp, reg): in place on wt and w (p/src/rhals.cpp:107-114). */
 int rnmf_gpu_rhals_update_W(rnmf_gpu_context* ctx, int dtype, int location,

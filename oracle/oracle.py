@@ -193,6 +193,26 @@ def rqb(a, target_rank, oversampling=20, power_iterations=2, test_matrix=1, seed
     return q, b
 
 
+def rqb_streaming(a, target_rank, oversampling=20, power_iterations=2, test_matrix=1, seed=0, block_size=1024,
+                  omega=None):
+    """rqb_streaming (p/src/sketch.cpp:73-116) over the in-memory matrix a, column blocks of block_size."""
+    a = _f64(a)
+    m, n = a.shape
+    lo = _I64(0)
+    e = err_buffer()
+    args = (_I64(m), _I64(n), _I64(target_rank), _I64(oversampling), _I64(power_iterations),
+            ctypes.c_int(int(test_matrix)), _I64(block_size), ctypes.c_uint64(seed))
+    st = lib().oracle_rqb_streaming(_dp(a), *args, None, None, None, ctypes.byref(lo), e, _CAP)
+    raise_for_status(st, e)
+    l = lo.value
+    q = np.empty((m, l))
+    b = np.empty((l, n))
+    om = _f64(omega) if omega is not None else None
+    st = lib().oracle_rqb_streaming(_dp(a), *args, _dp(om), _dp(q), _dp(b), ctypes.byref(lo), e, _CAP)
+    raise_for_status(st, e)
+    return q, b
+
+
 # ---- deterministic helpers -----------------------------------------------------------------
 def init_factors(x, rank, scheme=0, seed=0):
     x = _f64(x)

@@ -373,6 +373,63 @@ static SketchResult rqb(const Mat& a, const SketchOptions& o, const double* omeg
   return out;
 }
 
+// rqb_streaming: p/src/sketch.cpp:73-116 over an in-memory source read in column blocks of bs
+// (MatrixColumnSource, p/include/rnmf/sketch.hpp:41-51).  Blocks reduce in ascending order.
+static SketchResult rqb_streaming(const Mat& a, const SketchOptions& o, const double* omega) {
+  const Index m = a.r, n = a.c;
+  const Index l = sketch_width(m, n, o);
+  const Index bs = std::min(o.block_size, n);
+  Mat om;
+  if (omega) {
+    om = Mat::from(omega, n, l);
+  } else {
+    Rng rng(o.seed);
+    om = o.test_matrix == RNMF_TEST_UNIFORM ? uniform_matrix(n, l, rng) : gaussian_matrix(n, l, rng);
+  }
+  auto block = [&](Index c0, Index w) {  // read_columns(c0, w) + the finite check (:86-91)
+    Mat b(m, w);
+    for (Index i = 0; i < m; ++i)
+      for (Index j = 0; j < w; ++j) b(i, j) = a(i, c0 + j);
+    if (!all_finite(b))
+      throw DataError("rqb_streaming: non-finite values in columns [" + std::to_string(c0) + ", " +
+                      std::to_string(c0 + w) + ")");
+    return b;
+  };
+  auto rows_of = [&](const Mat& x, Index r0, Index cnt) {
+    Mat s(cnt, x.c);
+    for (Index i = 0; i < cnt; ++i)
+      for (Index j = 0; j < x.c; ++j) s(i, j) = x(r0 + i, j);
+    return s;
+  };
+  auto add_to = [](Mat& y, const Mat& t) {
+    for (size_t e = 0; e < y.a.size(); ++e) y.a[e] += t.a[e];
+  };
+  Mat y(m, l);
+  for (Index c0 = 0; c0 < n; c0 += bs) {
+    const Index w = std::min(bs, n - c0);
+    add_to(y, matmul(block(c0, w), rows_of(om, c0, w)));  // :95-97
+  }
+  for (Index it = 0; it < o.power_iterations; ++it) {  // :99-105
+    const Mat q = economic_qr(y).q;
+    y = Mat(m, l);
+    for (Index c0 = 0; c0 < n; c0 += bs) {
+      const Index w = std::min(bs, n - c0);
+      const Mat b = block(c0, w);
+      add_to(y, matmul(b, matmul_tn(b, q)));
+    }
+  }
+  SketchResult out;
+  out.q = economic_qr(y).q;  // :108
+  out.b = Mat(l, n);
+  for (Index c0 = 0; c0 < n; c0 += bs) {  // :109-113
+    const Index w = std::min(bs, n - c0);
+    const Mat bb = matmul_tn(out.q, block(c0, w));
+    for (Index i = 0; i < l; ++i)
+      for (Index j = 0; j < w; ++j) out.b(i, c0 + j) = bb(i, j);
+  }
+  return out;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Options / helpers: p/include/rnmf/hals.hpp:15-38,101-125 and p/src/hals.cpp:17-124.
 static constexpr double kDivisionFloor = 1e-12;  // hals.hpp:67
@@ -1188,6 +1245,24 @@ int oracle_rqb(const double* a, int64_t m, int64_t n, int64_t target_rank, int64
     *l_out = orc::sketch_width(m, n, so);
     if (!q_out && !b_out) return;
     auto s = orc::rqb(x, so, omega);
+    if (q_out) s.q.to(q_out);
+    if (b_out) s.b.to(b_out);
+  });
+}
+int oracle_rqb_streaming(const double* a, int64_t m, int64_t n, int64_t target_rank, int64_t oversampling,
+                         int64_t power_iterations, int test_matrix, int64_t block_size, uint64_t seed,
+                         const double* omega, double* q_out, double* b_out, int64_t* l_out, char* err, size_t cap) {
+  return guarded(err, cap, [&] {
+    orc::SketchOptions so;
+    so.target_rank = target_rank;
+    so.oversampling = oversampling;
+    so.power_iterations = power_iterations;
+    so.test_matrix = test_matrix;
+    so.block_size = block_size;
+    so.seed = seed;
+    *l_out = orc::sketch_width(m, n, so);
+    if (!q_out && !b_out) return;
+    auto s = orc::rqb_streaming(orc::Mat::from(a, m, n), so, omega);
     if (q_out) s.q.to(q_out);
     if (b_out) s.b.to(b_out);
   });

@@ -55,6 +55,12 @@ int oracle_rqb(const double* a, int64_t m, int64_t n, int64_t target_rank, int64
                int64_t power_iterations, int test_matrix, uint64_t seed, const double* omega,
                double* q_out, double* b_out, int64_t* l_out, char* err, size_t cap);
 
+/* rqb_streaming over an in-memory column source (p/src/sketch.cpp:73-116) */
+int oracle_rqb_streaming(const double* a, int64_t m, int64_t n, int64_t target_rank, int64_t oversampling,
+                         int64_t power_iterations, int test_matrix, int64_t block_size, uint64_t seed,
+                         const double* omega, double* q_out, double* b_out, int64_t* l_out, char* err,
+                         size_t cap);
+
 /* ---- deterministic HALS helpers (p/src/hals.cpp) ---- */
 int oracle_init_factors(const double* x, int64_t m, int64_t n, int64_t rank, int scheme,
                         uint64_t seed, double* w_out, double* h_out, char* err, size_t cap);

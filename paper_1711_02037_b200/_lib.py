@@ -20,6 +20,9 @@ _sz = ctypes.c_size_t
 _cp = ctypes.c_char_p
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
+# rnmf_column_reader: int (*)(void* user, int64_t first, int64_t count, double* dst)
+COLUMN_READER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.POINTER(ctypes.c_double))
 
 _SIGS = {
     "rnmf_version": (_i32, [_cp, _sz]),
@@ -54,6 +57,15 @@ _SIGS = {
         _i32,
         [_vp, _vp, _i32, _i32, _i64, _i64, _i64, _i64, _i64, _i32, ctypes.c_uint64, _dp, _i32, _vp, _vp, _i64p,
          _cp, _sz],
+    ),
+    "rnmf_gpu_rqb_streaming": (
+        _i32,
+        [_vp, COLUMN_READER, _vp, _i64, _i64, _i64, _i64, _i64, _i32, _i64, ctypes.c_uint64, _dp, _dp, _dp, _i64p,
+         _cp, _sz],
+    ),
+    "rnmf_gpu_rqb_streaming_file": (
+        _i32,
+        [_vp, _cp, _i64, _i64, _i64, _i32, _i64, ctypes.c_uint64, _dp, _dp, _dp, _i64p, _i64p, _i64p, _cp, _sz],
     ),
     "rnmf_gpu_rhals_update_W": (
         _i32,

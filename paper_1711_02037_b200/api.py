@@ -40,6 +40,7 @@ from ._abi import (
     err_buffer,
     raise_for_status,
 )
+from . import _lib as _lib_mod
 from ._lib import lib
 
 __all__ = [
@@ -47,7 +48,8 @@ __all__ = [
     "CompressedProblem", "SketchResult", "Context", "rhals_fit", "rhals_fit_compressed", "compress",
     "rhals_update_W", "rhals_update_H", "rqb", "last_stage_times", "device_count", "version",
     "ShapeError", "ParameterError", "DataError", "IoError", "InitScheme", "UpdateOrder",
-    "StoppingRule", "TestMatrixKind", "MathMode",
+    "StoppingRule", "TestMatrixKind", "MathMode", "ColumnSource", "MatrixColumnSource", "FileColumnSource",
+    "rqb_streaming", "write_matrix_bin",
 ]
 
 _CAP = ctypes.c_size_t(_abi.ERR_CAP)
@@ -380,6 +382,118 @@ def rqb(a, opts: SketchOptions, *, omega=None, ctx: Optional[Context] = None,
                             int(opts.oversampling), int(opts.power_iterations), int(opts.test_matrix),
                             ctypes.c_uint64(int(opts.seed) & 0xFFFFFFFFFFFFFFFF), _dptr(om), int(math_mode), _ptr(q), _ptr(b),
                             ctypes.byref(lo), e, _CAP)
+    raise_for_status(st, e)
+    return SketchResult(q, b)
+
+
+# ---- column-streamed sketch (rqb_streaming, p/src/sketch.cpp:73-116) -----------------------------
+class ColumnSource:
+    """rnmf::ColumnSource (p/include/rnmf/sketch.hpp:26-33): rows(), cols() and
+    read_columns(first, count, dst) filling dst (rows x count float64, row-major) with columns
+    [first, first + count)."""
+
+    def rows(self) -> int:
+        raise NotImplementedError
+
+    def cols(self) -> int:
+        raise NotImplementedError
+
+    def read_columns(self, first: int, count: int, dst: np.ndarray) -> None:
+        raise NotImplementedError
+
+
+class MatrixColumnSource(ColumnSource):
+    """rnmf::MatrixColumnSource (p/include/rnmf/sketch.hpp:41-51): an in-memory matrix."""
+
+    def __init__(self, a):
+        self.a = np.asarray(a, dtype=np.float64)
+        if self.a.ndim != 2:
+            raise ShapeError("MatrixColumnSource: expected a 2-D matrix")
+
+    def rows(self) -> int:
+        return int(self.a.shape[0])
+
+    def cols(self) -> int:
+        return int(self.a.shape[1])
+
+    def read_columns(self, first: int, count: int, dst: np.ndarray) -> None:
+        if first < 0 or count < 1 or first + count > self.cols():
+            raise ParameterError(f"read_columns: range [{first}, {first + count}) out of bounds for {self.cols()} columns")
+        dst[:, :] = self.a[:, first:first + count]
+
+
+class FileColumnSource(ColumnSource):
+    """rnmf::FileColumnSource (p/include/rnmf/data_io.hpp:32-45) over an RNMFMAT1 binary file.
+    rqb_streaming reads it natively (rnmf_gpu_rqb_streaming_file); the header is validated there
+    with the reference's messages."""
+
+    def __init__(self, path: str):
+        self.path = str(path)
+
+
+def write_matrix_bin(path: str, a) -> None:
+    """RNMFMAT1 writer (p/include/rnmf/data_io.hpp:12-15, write_matrix with MatrixFormat::Bin):
+    magic, rows / cols as little-endian u64, row-major little-endian float64 payload."""
+    a = np.ascontiguousarray(a, dtype="<f8")
+    with open(path, "wb") as f:
+        f.write(b"RNMFMAT1")
+        f.write(np.array([a.shape[0], a.shape[1]], dtype="<u8").tobytes())
+        f.write(a.tobytes())
+
+
+def rqb_streaming(src, opts: SketchOptions, *, omega=None, ctx: Optional[Context] = None) -> SketchResult:
+    """rnmf::rqb_streaming (p/src/sketch.cpp:73-116) on the GPU, fp64: the source is read in column
+    blocks of opts.block_size, 2 + power_iterations passes, each block streamed to the device while
+    the host reads the next.  Returns host float64 Q (m x l) and B (l x n)."""
+    c = _ctx_for(0, ctx)
+    e = err_buffer()
+    lo = ctypes.c_int64(0)
+    seed = ctypes.c_uint64(int(opts.seed) & 0xFFFFFFFFFFFFFFFF)
+    if isinstance(src, FileColumnSource):
+        path = src.path.encode()
+        mo, no = ctypes.c_int64(0), ctypes.c_int64(0)
+        args = (int(opts.target_rank), int(opts.oversampling), int(opts.power_iterations), int(opts.test_matrix),
+                int(opts.block_size), seed)
+        st = lib().rnmf_gpu_rqb_streaming_file(c.handle, path, *args, None, None, None, ctypes.byref(mo),
+                                               ctypes.byref(no), ctypes.byref(lo), e, _CAP)
+        raise_for_status(st, e)
+        m, n, l = mo.value, no.value, lo.value
+        om = _f64_host(omega, n, l, "omega") if omega is not None else None
+        q = np.empty((m, l), dtype=np.float64)
+        b = np.empty((l, n), dtype=np.float64)
+        st = lib().rnmf_gpu_rqb_streaming_file(c.handle, path, *args, _dptr(om), _dptr(q), _dptr(b),
+                                               ctypes.byref(mo), ctypes.byref(no), ctypes.byref(lo), e, _CAP)
+        raise_for_status(st, e)
+        return SketchResult(q, b)
+    if not isinstance(src, ColumnSource):
+        src = MatrixColumnSource(src)
+    m, n = int(src.rows()), int(src.cols())
+    failure = []
+
+    def _read(_user, first, count, dst):
+        try:
+            view = np.ctypeslib.as_array(dst, shape=(m * count,)).reshape(m, count)
+            src.read_columns(int(first), int(count), view)
+            return 0
+        except BaseException as exc:  # reported through the status, re-raised below
+            failure.append(exc)
+            return 1
+
+    reader = _lib_mod.COLUMN_READER(_read)
+    args = (int(opts.target_rank), int(opts.oversampling), int(opts.power_iterations), int(opts.test_matrix),
+            int(opts.block_size), seed)
+    st = lib().rnmf_gpu_rqb_streaming(c.handle, reader, None, m, n, *args, None, None, None, ctypes.byref(lo), e, _CAP)
+    raise_for_status(st, e)
+    l = lo.value
+    om = _f64_host(omega, n, l, "omega") if omega is not None else None
+    q = np.empty((m, l), dtype=np.float64)
+    b = np.empty((l, n), dtype=np.float64)
+    st = lib().rnmf_gpu_rqb_streaming(c.handle, reader, None, m, n, *args, _dptr(om), _dptr(q), _dptr(b),
+                                      ctypes.byref(lo), e, _CAP)
+    if failure and not isinstance(failure[0], Exception):
+        raise failure[0]
+    if st != 0 and failure and isinstance(failure[0], (ShapeError, ParameterError, DataError, IoError)):
+        raise failure[0]
     raise_for_status(st, e)
     return SketchResult(q, b)
 

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <random>
@@ -34,6 +35,9 @@ struct ParameterError : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
 struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
@@ -318,6 +322,24 @@ constexpr ncclDataType_t nccl_type() {
 }
 
 
+
+// ---- streaming sketch helpers (rqb_streaming) -------------------------------------------------
+// bad |= 1 when the m x w column block (pitch ld) holds a non-finite value (p/src/sketch.cpp:88-91)
+__global__ void block_finite_kernel(const double* __restrict__ blk, int64_t m, int64_t w, int64_t ld, int* bad) {
+  int found = 0;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m * w; e += int64_t(gridDim.x) * blockDim.x)
+    found |= !isfinite(blk[(e / w) * ld + e % w]);
+  if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+// y += t (count doubles)
+__global__ void add_inplace_kernel(double* __restrict__ y, const double* __restrict__ t, int64_t count) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x)
+    y[e] += t[e];
+}
+
+// Host column reader of the streaming sketch: first, count -> m x count row-major doubles
+using ColumnReadFn = std::function<void(int64_t first, int64_t count, double* dst)>;
+
 template <typename T>
 class Engine {
  public:
@@ -555,6 +577,118 @@ class Engine {
     allreduce(b, size_t(l) * n);  // B = Q^T X over all rows
     *q_out = qb;
     *b_out = b;
+  }
+
+  // rqb_streaming (p/src/sketch.cpp:73-116), fp64: X arrives from the host in column blocks of
+  // `bs` (ColumnSource::read_columns); 2 + q passes over the source, exactly as the reference:
+  //   Y = sum_b X_b Omega_b;  q x { Q = qr(Y); Y = sum_b X_b (X_b^T Q) };  Q = qr(Y);  B_b = Q^T X_b.
+  // Each block is copied from a pinned staging buffer (two, alternating: the host reads block
+  // b + 1 while the GPU works on block b), checked for non-finite values (DataError naming the
+  // block's column range, p/src/sketch.cpp:89-91) and consumed by the FFMA X-streaming kernels.
+  void rqb_streaming(const ColumnReadFn& read, int64_t m, int64_t n, int l, int64_t q_iters, int64_t bs,
+                     const double* omega_dev, double* q_host, double* b_host) {
+    static_assert(std::is_same<T, double>::value, "rqb_streaming is fp64");
+    const int64_t ldb = (bs + 1) / 2 * 2;  // 16-byte row pitch
+    double* blk = ctx_->d<double>("rs.blk", size_t(m) * size_t(ldb));
+    double* stage[2] = {ctx_->h<double>("rs.h0", size_t(m) * size_t(bs)), ctx_->h<double>("rs.h1", size_t(m) * size_t(bs))};
+    double* y = ctx_->d<double>("rs.y", size_t(m) * l);
+    double* yt = ctx_->d<double>("rs.yt", size_t(m) * l);
+    double* q = ctx_->d<double>("rs.q", size_t(m) * l);
+    double* z = ctx_->d<double>("rs.z", size_t(bs) * l);
+    double* b = ctx_->d<double>("rs.b", size_t(l) * size_t(n));
+    double* bt = ctx_->d<double>("rs.bt", size_t(l) * size_t(bs));
+    const int splits = xtw_default_splits(m, bs);
+    double* part = ctx_->d<double>("rs.part", size_t(splits) * size_t(bs) * l);
+    int* bad = ctx_->d<int>("rs.bad", 1);
+    int* hbad = ctx_->h<int>("rs.bad.h", 1);
+    const int64_t ws_len = tsqr_workspace_doubles(m, l, ctx_->max_smem);
+    double* ws = ctx_->d<double>("tsqr.ws", size_t(ws_len));
+    double* cqws = ctx_->d<double>("cq.ws", size_t(cholqr_workspace_doubles(m, l)));
+    int* cqflag = ctx_->d<int>("cq.flag", 1);
+    int* hflag = ctx_->h<int>("cq.flag.h", 1);
+    cudaEvent_t copied[2];
+    for (auto& e : copied) RNMF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        for (int i = 0; i < 2; ++i) cudaEventDestroy(e[i]);
+      }
+    } evg{copied};
+    auto qr = [&](const double* a, double* out) {
+      tm_.span(kQr, [&] {
+        tm_.launches += launch_cholqr2<double>(a, m, l, out, cqws, cqflag, st_, nullptr);
+        RNMF_CUDA(cudaMemcpyAsync(hflag, cqflag, sizeof(int), cudaMemcpyDeviceToHost, st_));
+        RNMF_CUDA(cudaStreamSynchronize(st_));
+        if (hflag[0] != 0) tm_.launches += launch_tsqr<double>(a, m, l, out, ws, ctx_->max_smem, st_);
+      });
+    };
+    const int64_t nb = (n + bs - 1) / bs;
+    const double xbytes = double(m) * double(n) * sizeof(double);
+    // one pass over the source: fn(c0, w) enqueues the block's kernels
+    auto each_block = [&](auto&& fn) {
+      read(0, std::min(bs, n), stage[0]);
+      for (int64_t ib = 0; ib < nb; ++ib) {
+        const int64_t c0 = ib * bs, w = std::min(bs, n - c0);
+        double* hs = stage[ib & 1];
+        RNMF_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st_));
+        RNMF_CUDA(cudaMemcpy2DAsync(blk, size_t(ldb) * sizeof(double), hs, size_t(w) * sizeof(double),
+                                    size_t(w) * sizeof(double), size_t(m), cudaMemcpyHostToDevice, st_));
+        RNMF_CUDA(cudaEventRecord(copied[ib & 1], st_));
+        block_finite_kernel<<<int(std::min<int64_t>(148 * 4, std::max<int64_t>(1, (m * w + 255) / 256))), 256, 0, st_>>>(
+            blk, m, w, ldb, bad);
+        RNMF_CUDA_LAUNCH();
+        RNMF_CUDA(cudaMemcpyAsync(hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st_));
+        tm_.launches += 1;
+        fn(c0, w);
+        if (ib + 1 < nb) {
+          // the other staging buffer is free once its previous H2D copy has run
+          RNMF_CUDA(cudaEventSynchronize(copied[(ib + 1) & 1]));
+          const int64_t c1 = c0 + bs;
+          read(c1, std::min(bs, n - c1), stage[(ib + 1) & 1]);
+        }
+        RNMF_CUDA(cudaStreamSynchronize(st_));
+        if (hbad[0] != 0)
+          throw DataError("rqb_streaming: non-finite values in columns [" + std::to_string(c0) + ", " +
+                          std::to_string(c0 + w) + ")");
+      }
+      sketch_bytes_ += xbytes;
+      sketch_passes_ += 1;
+    };
+    auto add = [&](double* dst, const double* src, int64_t count) {
+      add_inplace_kernel<<<int(std::min<int64_t>(148 * 4, std::max<int64_t>(1, (count + 255) / 256))), 256, 0, st_>>>(
+          dst, src, count);
+      RNMF_CUDA_LAUNCH();
+      tm_.launches += 1;
+    };
+    tm_.span(kXw, [&] {
+      RNMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m) * l, st_));
+      each_block([&](int64_t c0, int64_t w) {
+        tm_.launches += launch_xw<double>(blk, m, w, ldb, omega_dev + c0 * l, l, yt, st_);
+        add(y, yt, m * l);
+      });
+    });
+    for (int64_t it = 0; it < q_iters; ++it) {
+      qr(y, q);
+      tm_.span(kXtw, [&] {
+        RNMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(m) * l, st_));
+        each_block([&](int64_t, int64_t w) {
+          tm_.launches += launch_xtw<double>(blk, m, w, ldb, q, l, part, splits, z, false, st_);  // Z = X_b^T Q
+          tm_.launches += launch_xw<double>(blk, m, w, ldb, z, l, yt, st_);                     // X_b Z
+          add(y, yt, m * l);
+        });
+      });
+    }
+    qr(y, q);
+    tm_.span(kXtw, [&] {
+      each_block([&](int64_t c0, int64_t w) {
+        tm_.launches += launch_xtw<double>(blk, m, w, ldb, q, l, part, splits, bt, true, st_);  // Q^T X_b (l x w)
+        RNMF_CUDA(cudaMemcpy2DAsync(b + c0, size_t(n) * sizeof(double), bt, size_t(w) * sizeof(double),
+                                    size_t(w) * sizeof(double), size_t(l), cudaMemcpyDeviceToDevice, st_));
+      });
+    });
+    RNMF_CUDA(cudaMemcpyAsync(q_host, q, sizeof(double) * size_t(m) * l, cudaMemcpyDeviceToHost, st_));
+    RNMF_CUDA(cudaMemcpyAsync(b_host, b, sizeof(double) * size_t(l) * size_t(n), cudaMemcpyDeviceToHost, st_));
+    RNMF_CUDA(cudaStreamSynchronize(st_));
   }
 
   // Full-space metrics (p/src/rhals.cpp:140-148) of the device factors w (m x k), h (k x n):
@@ -1270,6 +1404,91 @@ static void rqb_impl(rnmf_gpu_context* ctx, const void* a_in, int location, int6
   ctx->last.sketch_passes = eng.sketch_passes_;
 }
 
+// ---- FileColumnSource (p/src/data_io.cpp:185-223): RNMFMAT1 binary matrix, read by column blocks
+// (one strided read per row, as the reference).  Header validated up front with the reference's
+// messages.
+class FileColumns {
+ public:
+  explicit FileColumns(const std::string& path) : path_(path) {
+    f_ = std::fopen(path.c_str(), "rb");
+    if (!f_) throw IoError("cannot open '" + path + "'");
+    char magic[8] = {};
+    const size_t got = std::fread(magic, 1, 8, f_);
+    if (got != 8 || std::memcmp(magic, "RNMFMAT1", 8) != 0)
+      throw DataError("'" + path + "': bad magic at byte 0 (expected \"RNMFMAT1\")");
+    unsigned char hdr[16];
+    if (std::fread(hdr, 1, 16, f_) != 16) throw DataError("'" + path + "': truncated header, file ends before byte 24");
+    uint64_t rows = 0, cols = 0;
+    for (int i = 7; i >= 0; --i) rows = (rows << 8) | hdr[i];
+    for (int i = 7; i >= 0; --i) cols = (cols << 8) | hdr[8 + i];
+    std::fseek(f_, 0, SEEK_END);
+    const uint64_t size = uint64_t(std::ftell(f_));
+    const uint64_t expected = 24 + rows * cols * sizeof(double);
+    if (size != expected)
+      throw DataError("'" + path + "': file is " + std::to_string(size) + " bytes, expected " + std::to_string(expected) +
+                      " for a " + std::to_string(rows) + "x" + std::to_string(cols) + " matrix");
+    rows_ = int64_t(rows);
+    cols_ = int64_t(cols);
+  }
+  ~FileColumns() {
+    if (f_) std::fclose(f_);
+  }
+  int64_t rows() const { return rows_; }
+  int64_t cols() const { return cols_; }
+  void read_columns(int64_t first, int64_t count, double* dst) {
+    for (int64_t i = 0; i < rows_; ++i) {
+      const uint64_t off = 24 + (uint64_t(i) * uint64_t(cols_) + uint64_t(first)) * sizeof(double);
+      if (std::fseek(f_, long(off), SEEK_SET) != 0 ||
+          std::fread(dst + i * count, sizeof(double), size_t(count), f_) != size_t(count))
+        throw IoError("'" + path_ + "': read failed for columns [" + std::to_string(first) + ", " +
+                      std::to_string(first + count) + ") at row " + std::to_string(i));
+    }
+  }
+
+ private:
+  std::string path_;
+  std::FILE* f_ = nullptr;
+  int64_t rows_ = 0, cols_ = 0;
+};
+
+static void rqb_streaming_impl(rnmf_gpu_context* ctx, const ColumnReadFn& read, int64_t m, int64_t n, int64_t rank,
+                               int64_t p, int64_t qi, int test_matrix, int64_t block_size, uint64_t seed,
+                               const double* omega, double* q_out, double* b_out, int64_t* l_out) {
+  ctx->last = rnmf_stage_times{};
+  Timer tm(ctx);
+  Engine<double> eng(ctx, tm);
+  const int64_t l64 = sketch_width(m, n, rank, p, qi);  // p/src/sketch.cpp:30-50 (+ the block size check)
+  if (block_size < 1) throw ParameterError("sketch: block size must be at least 1");
+  if (l_out) *l_out = l64;
+  if (!q_out && !b_out) {
+    tm.finish(ctx->last);
+    return;
+  }
+  if (!q_out || !b_out) throw ParameterError("rqb_streaming: q_out and b_out must both be given");
+  const int l = int(l64);
+  if (l > tsqr_max_l(ctx->max_smem) || l > 128)
+    throw ParameterError("B200 path: sketch width " + std::to_string(l) + " above the supported maximum");
+  const int64_t bs = std::min(block_size, n);
+  // Omega from Rng(seed) directly (p/src/sketch.cpp:79-80), row-major n x l
+  std::vector<double> om_host;
+  const double* om = omega;
+  if (!om) {
+    om_host.resize(size_t(n) * l);
+    Rng rng(seed);
+    if (test_matrix == RNMF_TEST_UNIFORM)
+      fill_uniform(rng, om_host.data(), om_host.size());
+    else
+      fill_gaussian(rng, om_host.data(), om_host.size());
+    om = om_host.data();
+  }
+  const double* om_dev = eng.upload_converted("omega", om, size_t(n) * l);
+  tm.span(kSketch, [&] { eng.rqb_streaming(read, m, n, l, qi, bs, om_dev, q_out, b_out); });
+  tm.finish(ctx->last);
+  ctx->last.sketch_bytes = eng.sketch_bytes_;
+  ctx->last.sketch_passes = eng.sketch_passes_;
+}
+
+
 // Stage API: rhals_update_W / rhals_update_H on a caller-supplied compressed problem, and the
 // fit loop started from one.
 template <typename T>
@@ -1402,6 +1621,9 @@ int guarded(char* err, size_t cap, F&& f) {
   } catch (const rnmf_gpu::DataError& e) {
     put_err(err, cap, e.what());
     return RNMF_DATA_ERROR;
+  } catch (const rnmf_gpu::IoError& e) {
+    put_err(err, cap, e.what());
+    return RNMF_IO_ERROR;
   } catch (const std::exception& e) {
     put_err(err, cap, e.what());
     return RNMF_CUDA_ERROR;
@@ -1665,6 +1887,44 @@ int rnmf_gpu_rqb(rnmf_gpu_context* ctx, const void* a, int dtype, int location, 
     else
       rqb_impl<double>(ctx, a, location, m, n, target_rank, oversampling, power_iterations, test_matrix, seed, omega,
                        math_mode, q_out, b_out, l_out);
+  });
+}
+
+int rnmf_gpu_rqb_streaming(rnmf_gpu_context* ctx, rnmf_column_reader reader, void* user, int64_t m, int64_t n,
+                           int64_t target_rank, int64_t oversampling, int64_t power_iterations, int test_matrix,
+                           int64_t block_size, uint64_t seed, const double* omega, double* q_out, double* b_out,
+                           int64_t* l_out, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    if (!reader) throw rnmf_gpu::ParameterError("rqb_streaming: reader is NULL");
+    if (m < 0 || n < 0) throw rnmf_gpu::ShapeError("rqb_streaming: negative dimensions " + rnmf_gpu::shape_string(m, n));
+    DeviceGuard g(ctx->device);
+    const rnmf_gpu::ColumnReadFn read = [&](int64_t first, int64_t count, double* dst) {
+      if (reader(user, first, count, dst) != 0)
+        throw rnmf_gpu::IoError("read_columns: the column source failed for columns [" + std::to_string(first) + ", " +
+                                std::to_string(first + count) + ")");
+    };
+    rnmf_gpu::rqb_streaming_impl(ctx, read, m, n, target_rank, oversampling, power_iterations, test_matrix, block_size,
+                                 seed, omega, q_out, b_out, l_out);
+  });
+}
+
+int rnmf_gpu_rqb_streaming_file(rnmf_gpu_context* ctx, const char* path, int64_t target_rank, int64_t oversampling,
+                                int64_t power_iterations, int test_matrix, int64_t block_size, uint64_t seed,
+                                const double* omega, double* q_out, double* b_out, int64_t* m_out, int64_t* n_out,
+                                int64_t* l_out, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    if (!path) throw rnmf_gpu::ParameterError("rqb_streaming: path is NULL");
+    rnmf_gpu::FileColumns src(path);
+    if (m_out) *m_out = src.rows();
+    if (n_out) *n_out = src.cols();
+    DeviceGuard g(ctx->device);
+    const rnmf_gpu::ColumnReadFn read = [&](int64_t first, int64_t count, double* dst) {
+      src.read_columns(first, count, dst);
+    };
+    rnmf_gpu::rqb_streaming_impl(ctx, read, src.rows(), src.cols(), target_rank, oversampling, power_iterations,
+                                 test_matrix, block_size, seed, omega, q_out, b_out, l_out);
   });
 }
 

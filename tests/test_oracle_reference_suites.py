@@ -402,3 +402,39 @@ def test_errors_in_reference_order(oracle):  # p/src/hals.cpp:36-53: data errors
                dict(rank=2, reg=(-1, 0, 0, 0)), dict(rank=2, trace_full_every=0), dict(rank=2, oversampling=-1)):
         with pytest.raises(ParameterError):
             oracle.rhals_fit(y, o_opts(oracle, **kw))
+
+
+def test_oracle_rqb_streaming_block_independence(oracle):
+    """p/tests/test_sketch.cpp:143-166 on the oracle's restatement of rqb_streaming."""
+    a = oracle.synth_lowrank(300, 200, 5, 0.0, 5)
+    a /= np.linalg.norm(a)
+    qm, bm = oracle.rqb(a, 5, 10, 2, seed=21)
+    prev = None
+    for bs in (1, 7, 64, 1024):
+        q, b = oracle.rqb_streaming(a, 5, 10, 2, seed=21, block_size=bs)
+        assert np.linalg.norm(q @ b - qm @ bm) <= 1e-10
+        if prev is not None:
+            assert np.linalg.norm(q @ b - prev) <= 1e-10
+        prev = q @ b
+
+
+def test_oracle_rqb_streaming_errors(oracle):
+    a = oracle.synth_lowrank(50, 80, 3, 0.0, 1)
+    a[3, 70] = np.inf
+    with pytest.raises(DataError, match=r"non-finite values in columns \[64, 80\)"):
+        oracle.rqb_streaming(a, 3, 2, 1, block_size=32)
+    with pytest.raises(ParameterError, match="block size"):
+        oracle.rqb_streaming(a, 3, 2, 1, block_size=0)
+
+
+def test_rnmfmat1_writer_layout(tmp_path):
+    """RNMFMAT1 (p/include/rnmf/data_io.hpp:12-15): magic, LE u64 rows / cols, row-major LE f64."""
+    from paper_1711_02037_b200 import api
+
+    a = np.arange(6, dtype=np.float64).reshape(2, 3)
+    p = tmp_path / "a.bin"
+    api.write_matrix_bin(str(p), a)
+    raw = p.read_bytes()
+    assert raw[:8] == b"RNMFMAT1" and len(raw) == 24 + 48
+    assert int.from_bytes(raw[8:16], "little") == 2 and int.from_bytes(raw[16:24], "little") == 3
+    assert np.array_equal(np.frombuffer(raw[24:], dtype="<f8").reshape(2, 3), a)
