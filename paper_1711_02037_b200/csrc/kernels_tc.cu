@@ -909,8 +909,10 @@ __global__ void tc_prep_rows_kernel(const float* __restrict__ src, int c, int64_
   }
 }
 
-// projected grad_W partial sums (projected_sq_norm, p/src/hals.cpp:55-65): one row per thread
-constexpr int kPgwThreads = 256;
+// projected grad_W partial sums (projected_sq_norm, p/src/hals.cpp:55-65): one row per thread, the
+// row's W and X H^T entries in registers (KP >= k), H H^T broadcast from shared memory
+constexpr int kPgwThreads = 128;
+template <int KP>
 __global__ void __launch_bounds__(kPgwThreads) tc_pgw_kernel(const float* __restrict__ xht, const float* __restrict__ w,
                                                              int64_t m, int k, const double* __restrict__ hht,
                                                              double* __restrict__ part) {
@@ -919,13 +921,17 @@ __global__ void __launch_bounds__(kPgwThreads) tc_pgw_kernel(const float* __rest
   __syncthreads();
   double acc = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
-    const float* wr = w + i * k;
-    const float* xr = xht + i * k;
+    double wv[KP];
+#pragma unroll
+    for (int p = 0; p < KP; ++p) wv[p] = p < k ? double(w[i * k + p]) : 0.0;
+#pragma unroll 1
     for (int j = 0; j < k; ++j) {
       double whh = 0.0;
-      for (int p = 0; p < k; ++p) whh = fma(double(wr[p]), sh[p * k + j], whh);
-      const double g = -2.0 * (double(xr[j]) - whh);
-      const double gi = wr[j] > 0.f ? g : fmin(0.0, g);
+#pragma unroll
+      for (int p = 0; p < KP; ++p)
+        if (p < k) whh = fma(wv[p], sh[p * k + j], whh);
+      const double g = -2.0 * (double(xht[i * k + j]) - whh);
+      const double gi = w[i * k + j] > 0.f ? g : fmin(0.0, g);
       acc = fma(gi, gi, acc);
     }
   }
@@ -998,18 +1004,24 @@ int launch_tc_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const flo
   return 1;
 }
 
-int tc_pgw_blocks(int64_t m) { return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kPgwThreads), 148 * 4))); }
+int tc_pgw_blocks(int64_t m) { return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, kPgwThreads), 148 * 8))); }
 
 int launch_tc_pgw(const float* xht, const float* w, int64_t m, int k, const double* hht, double* part_pgw,
                   int* nblocks, cudaStream_t stream) {
   const int blocks = tc_pgw_blocks(m);
   const size_t smem = sizeof(double) * (size_t(k) * k + kPgwThreads / 32);
-  tc_pgw_kernel<<<blocks, kPgwThreads, smem, stream>>>(xht, w, m, k, hht, part_pgw);
+  if (k <= 16)
+    tc_pgw_kernel<16><<<blocks, kPgwThreads, smem, stream>>>(xht, w, m, k, hht, part_pgw);
+  else if (k <= 32)
+    tc_pgw_kernel<32><<<blocks, kPgwThreads, smem, stream>>>(xht, w, m, k, hht, part_pgw);
+  else if (k <= 48)
+    tc_pgw_kernel<48><<<blocks, kPgwThreads, smem, stream>>>(xht, w, m, k, hht, part_pgw);
+  else
+    tc_pgw_kernel<64><<<blocks, kPgwThreads, smem, stream>>>(xht, w, m, k, hht, part_pgw);
   RNMF_CUDA_LAUNCH();
   *nblocks = blocks;
   return 1;
 }
-
 
 // ================================================================================================
 // Fused metrics pass for k <= 32 (tc_metrics.h launch_tc_xht_resid): ONE read of X gives both
