@@ -148,6 +148,8 @@ typedef struct rnmf_stage_times {
   int64_t xtw_launches;
   double xw_bytes;
   double xtw_bytes;
+  double xw_kernel_ms;     /* the X*S GEMM kernels alone (xw_ms minus operand prep) */
+  double xtw_kernel_ms;    /* the X^T*S GEMM kernels alone (xtw_ms minus operand prep and split reduction) */
 } rnmf_stage_times;
 
 typedef struct rnmf_gpu_context rnmf_gpu_context;

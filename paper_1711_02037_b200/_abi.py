@@ -170,6 +170,8 @@ class StageTimesC(ctypes.Structure):
         ("xtw_launches", ctypes.c_int64),
         ("xw_bytes", ctypes.c_double),
         ("xtw_bytes", ctypes.c_double),
+        ("xw_kernel_ms", ctypes.c_double),
+        ("xtw_kernel_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -193,7 +193,7 @@ struct rnmf_gpu_context {
 namespace rnmf_gpu {
 
 // ---- stage timing -----------------------------------------------------------------------------
-enum Stage { kScan, kSketch, kQr, kInit, kSweeps, kMetrics, kXw, kXtw, kH2D, kD2H, kNumStages };
+enum Stage { kScan, kSketch, kQr, kInit, kSweeps, kMetrics, kXw, kXtw, kH2D, kD2H, kXwK, kXtwK, kNumStages };
 
 struct Timer {
   rnmf_gpu_context* ctx;
@@ -246,6 +246,8 @@ struct Timer {
     out.xtw_ms = acc[kXtw];
     out.xw_launches = counts[kXw];
     out.xtw_launches = counts[kXtw];
+    out.xw_kernel_ms = acc[kXwK];
+    out.xtw_kernel_ms = acc[kXtwK];
     out.total_ms = tot;
     out.kernel_launches = launches;
   }
@@ -497,7 +499,7 @@ class Engine {
         if constexpr (std::is_same<T, float>::value) {
           if (tc) {
             tm_.launches += launch_tc_prep_st(s, n, l, st_hi, st_lo, st_);
-            tm_.launches += launch_tc_xw(x, m, n, ldx, st_hi, st_lo, l, out, x3, ctx_->sm_count, st_);
+            tm_.span(kXwK, [&] { tm_.launches += launch_tc_xw(x, m, n, ldx, st_hi, st_lo, l, out, x3, ctx_->sm_count, st_); });
             return;
           }
         }
@@ -506,9 +508,9 @@ class Engine {
         // and the RNMF_XW_LEGACY testing knob: the register-staged kernel
         if (sizeof(T) == 4 && !std::getenv("RNMF_XW_LEGACY")) {
           T* spad = ctx_->d<T>("rqb.spad", size_t(xw_tma_spad_len(n, l)));
-          tm_.launches += launch_xw_tma<T>(x, m, n, ldx, s, l, out, spad, ctx_->sm_count, st_);
+          tm_.span(kXwK, [&] { tm_.launches += launch_xw_tma<T>(x, m, n, ldx, s, l, out, spad, ctx_->sm_count, st_); });
         } else {
-          tm_.launches += launch_xw<T>(x, m, n, ldx, s, l, out, st_);
+          tm_.span(kXwK, [&] { tm_.launches += launch_xw<T>(x, m, n, ldx, s, l, out, st_); });
         }
       });
       sketch_bytes_ += xbytes;
@@ -520,7 +522,9 @@ class Engine {
         if constexpr (std::is_same<T, float>::value) {
           if (tc) {
             tm_.launches += launch_tc_prep_st(s, m, l, st_hi, st_lo, st_);
-            tm_.launches += launch_tc_xtw(x, m, n, ldx, st_hi, st_lo, l, part, splits, x3, ctx_->sm_count, st_);
+            tm_.span(kXtwK, [&] {
+              tm_.launches += launch_tc_xtw(x, m, n, ldx, st_hi, st_lo, l, part, splits, x3, ctx_->sm_count, st_);
+            });
             tm_.launches += launch_splitk_reduce<T>(part, splits, n, l, out, tr, st_);
             return;
           }
@@ -529,9 +533,12 @@ class Engine {
           const int sp = xtw_tma_splits(m, n, ctx_->sm_count);
           T* part2 = ctx_->d<T>("rqb.part2", size_t(sp) * n * l);
           T* spad = ctx_->d<T>("rqb.spad2", size_t(xw_tma_spad_len(m, l)));
-          tm_.launches += launch_xtw_tma<T>(x, m, n, ldx, s, l, part2, sp, out, tr, spad, ctx_->sm_count, st_);
+          // (the FFMA path's span includes its fixed-order split reduction)
+          tm_.span(kXtwK, [&] {
+            tm_.launches += launch_xtw_tma<T>(x, m, n, ldx, s, l, part2, sp, out, tr, spad, ctx_->sm_count, st_);
+          });
         } else {
-          tm_.launches += launch_xtw<T>(x, m, n, ldx, s, l, part, splits, out, tr, st_);
+          tm_.span(kXtwK, [&] { tm_.launches += launch_xtw<T>(x, m, n, ldx, s, l, part, splits, out, tr, st_); });
         }
       });
       sketch_bytes_ += xbytes;
