@@ -404,6 +404,12 @@ def main():
                                                "total_ms")},
         "stage_share": shares,
         "sweep_us": 1e3 * agg["sweeps_ms"] / max(sweeps, 1),
+        # sweeps/s steady state (sweep kernel only, no full-space metrics) and amortised
+        # (whole fit), and the W-phase column step (sweep time / k, an upper bound: it includes the
+        # per-sweep H phase and compressed evaluation)
+        "sweeps_per_s_steady": sweeps / (agg["sweeps_ms"] / 1e3) if agg["sweeps_ms"] > 0 else None,
+        "sweeps_per_s_amortised": sweeps / (agg["total_ms"] / 1e3) if agg["total_ms"] > 0 else None,
+        "column_step_us_upper": 1e3 * agg["sweeps_ms"] / max(sweeps, 1) / k,
         "final_rel_err": last.trace[-1].rel_err,
         "wall_s_timed": wall_s,
         "clocks": clocks,

@@ -172,3 +172,31 @@ def test_sharded_default_streams_and_errors(oracle):
             d.rhals_fit_sharded(x, opts, row_offset=10, m_total=x.shape[0], ctx=ctx)
     finally:
         ctx.close()
+
+
+@pytest.mark.gpu
+def test_sharded_world1_tf32x3(oracle):
+    """Row-sharded entry at world 1 with the tensor-core math mode: the sharded branches of the
+    tcgen05 sketch and metrics (NCCL all-reduce of the X^T W partial, of the objective and grad_W
+    sums) against the plain fit and the oracle."""
+    from paper_1711_02037_b200 import api, distributed as d
+
+    x, omega, wi, hi = _problem(m=900, n=200)
+    x = x.astype(np.float32)
+    opts = api.SolverOptions(rank=6, oversampling=4, power_iterations=1, max_iter=25, tol=1e-300, seed=0,
+                             trace_full_every=5)
+    opts.math_mode = api.MathMode.TF32x3
+    ctx = d.ShardedContext(0, rank=0, world=1, comm_id=d.comm_unique_id())
+    try:
+        res = d.rhals_fit_sharded(x, opts, row_offset=0, m_total=x.shape[0], ctx=ctx, omega=omega, w0=wi, h0=hi)
+        plain = api.rhals_fit(x, opts, omega=omega, w0=wi, h0=hi)
+    finally:
+        ctx.close()
+    ref = oracle.rhals_fit(x.astype(np.float64), dict(rank=6, oversampling=4, power_iterations=1, max_iter=25,
+                                                       tol=1e-300, seed=0, trace_full_every=5),
+                           omega=omega, w0=wi, h0=hi)
+    for g, p, o in zip(res.trace, plain.trace, ref.trace):
+        for f in ("objective", "rel_err", "objective_compressed"):
+            np.testing.assert_allclose(getattr(g, f), o[f], rtol=1e-3, err_msg=f"{f} @ {g.iter}")
+            np.testing.assert_allclose(getattr(g, f), getattr(p, f), rtol=1e-6)
+    assert abs(res.trace[-1].rel_err - ref.trace[-1]["rel_err"]) < 1e-4
