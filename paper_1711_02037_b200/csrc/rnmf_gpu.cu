@@ -1011,6 +1011,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     }
     int extra = 0;
     int64_t tb = t_begin;
+    bool speculative = false;
     while (true) {
       a.flags = kRecord | kDoW | kDoH | (o.reseed_dead ? kReseed : 0) | extra |
                 (first ? (kEval0 | kInitWn | (io.init_wt ? kInitWt : 0)) : 0);
@@ -1020,6 +1021,12 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
       tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
       RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 3 * sizeof(long long), cudaMemcpyDeviceToHost, st));
       if (prof) RNMF_CUDA(cudaMemcpyAsync(hprof, a.prof, kSweepProfSlots * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      // Without reseed_dead the launch never hands control back mid-chunk, so the full-space metrics
+      // of the launch's final factors are enqueued before waiting for its status: the GPU goes
+      // straight from the sweep kernel into the metrics passes (the record is dropped below if the
+      // launch turned out to be a stationary start, last < t_begin).
+      speculative = !o.reseed_dead && extra == 0;
+      if (speculative) eng.metrics(k, io.w, io.h, mres + 2 * eval_iter.size(), a.vm);
       RNMF_CUDA(cudaStreamSynchronize(st));
       if (prof)
         for (int i = 0; i < kSweepProfSlots; ++i) prof_sum[size_t(i)] += hprof[i];
@@ -1052,7 +1059,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
     last = hstat[0];
     const bool stopped = hstat[1] != 0;
     if (last >= t_begin) {
-      eng.metrics(k, io.w, io.h, mres + 2 * eval_iter.size(), a.vm);  // V = H H^T of the final H
+      if (!speculative) eng.metrics(k, io.w, io.h, mres + 2 * eval_iter.size(), a.vm);  // V = H H^T of the final H
       eval_iter.push_back(last);
     }
     bool stop = stopped;
