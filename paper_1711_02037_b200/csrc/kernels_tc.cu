@@ -609,11 +609,25 @@ CUtensorMap make_tma_2d(const void* base, int elem_bytes, int64_t rows, int64_t 
   return m;
 }
 
+// Row splits of X^T S: the (column tile, split) units are spread over the persistent CTAs, so pick
+// the split count whose unit count fills the last round best (units / (rounds * CTAs)), with at
+// least 4 K stages (128 rows) per unit; near-ties go to fewer splits (less partial traffic).
+// E.g. C4 (157 column tiles): 8 splits, 94 % of 9 rounds, instead of 1 split and 53 % of 2 rounds.
 int tc_xtw_splits(int64_t m, int64_t n, int sm_count) {
   const int64_t ct = ceil_div(n, 128);
-  int64_t s = std::max<int64_t>(1, sm_count / ct);
-  s = std::min<int64_t>(s, std::max<int64_t>(1, m / (4 * kBK)));
-  return int(s);
+  const int64_t G = std::max(sm_count, 1);
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(256, m / (4 * kBK)));
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t s = 1; s <= smax; ++s) {
+    const int64_t units = ct * s;
+    const double eff = double(units) / double(ceil_div(units, G) * G);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return int(best);
 }
 
 int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int c,
