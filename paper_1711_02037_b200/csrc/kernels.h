@@ -177,6 +177,7 @@ enum SweepFlags : int {
   kColOrdered = 128,  // column-step reduction through ordered fp64 partials (else fixed-point atomics)
   kReseed = 256,      // reseed_dead: liveness stamps per sweep, stop at a dead component (host reseeds)
   kEvalPrev = 512,    // evaluate + record sweep t_begin - 1 first (after a host-side reseed)
+  kXFlat = 1024,      // row-sharded column step: every CTA exchanges with every GPU (testing knob)
 };
 // Sync block of the sweep kernel (zeroed before every launch): the legacy grid-barrier counter at
 // byte 0 (cross-GPU counter at byte 64), a 3-slot ring of 64-bit fixed-point accumulators for the
@@ -191,8 +192,15 @@ constexpr int kColAccReps = 4;       // accumulator replicas per entry
 constexpr int kColAccStride = kColAccReps * kColAccMax * kColAccSpacing;  // words per slot
 constexpr int kBarReps = 8;          // grid-barrier counter replicas (one 128-byte line each)
 constexpr size_t kSweepBarOffset = 128 + 3 * size_t(kColAccStride) * sizeof(unsigned long long);
-// zeroed part: counters (bytes 0 / 64), accumulators, replicated barrier counters
-constexpr size_t kSweepSyncBytes = kSweepBarOffset + size_t(kBarReps) * 128;
+// Row-sharded column step (hierarchical): every GPU's CTA 0 adds its GPU's column sums into every
+// GPU's global accumulators (3-slot ring, one line per entry), arrives on every GPU's CTA-0
+// counter, and releases its own GPU's CTAs through the flag.
+constexpr size_t kSweepGaccOffset = kSweepBarOffset + size_t(kBarReps) * 128;
+constexpr size_t kSweepXcolOffset = kSweepGaccOffset + 3 * size_t(kColAccMax) * kColAccSpacing * sizeof(unsigned long long);
+constexpr size_t kSweepFlagOffset = kSweepXcolOffset + 128;
+// zeroed part: counters (bytes 0 / 64), accumulators, replicated barrier counters, the sharded
+// column-step accumulators / counter / flag
+constexpr size_t kSweepSyncBytes = kSweepFlagOffset + 128;
 // Row-sharded runs (one process per GPU): after the zeroed part, a 2-slot exchange buffer of
 // kMaxWorld x kXMax doubles per slot that peers write into (never needs clearing).
 constexpr int kMaxWorld = 8;
@@ -259,6 +267,8 @@ struct SweepPlan {
 template <typename T>
 SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem);
 template <typename T>
-int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream);
+// zero_sync = false: the caller has zeroed the sync block (row-sharded runs zero it, then pass an
+// NCCL all-reduce so no GPU's kernel can touch a peer's block before the peer zeroed it)
+int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream, bool zero_sync = true);
 
 }  // namespace rnmf_gpu

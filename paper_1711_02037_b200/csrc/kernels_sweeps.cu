@@ -436,6 +436,10 @@ struct Sweeper {
     const int64_t slot0 = (cstep % 3) * kColAccStride;
     const int64_t off = slot0 + (int64_t(g % kColAccReps) * kColAccMax + tid) * kColAccSpacing;
     unsigned long long* cur = colacc + off;
+    if (sharded() && !(a.flags & kXFlat)) {
+      col_allreduce_xgpu(L1, v, sc, inv, slot0, off, wr);
+      return;
+    }
     if (tid < L1) {
       const long long fx = __double2ll_rn(v * sc[tid < l ? 0 : 1]);  // exact power-of-two scaling
       if (sharded()) {
@@ -464,6 +468,66 @@ struct Sweeper {
       for (int rp = 0; rp < kColAccReps; ++rp)
         acc += ld_cg(colacc + slot0 + (int64_t(rp) * kColAccMax + tid) * kColAccSpacing);
       const long long sum = static_cast<long long>(acc);
+      wr(tid, double(sum) * inv[tid < l ? 0 : 1]);
+    }
+    ++cstep;
+    prof_tick(kPfReduce1);
+  }
+
+  // Row-sharded column step, hierarchical: (1) every CTA adds its fixed-point partials into this
+  // GPU's replicated accumulators, (2) local grid barrier, (3) CTA 0 sums the replicas and adds the
+  // GPU's sums into every GPU's global accumulators (world remote adds per entry), arrives on every
+  // GPU's CTA-0 counter and waits for all world arrivals on its own, then releases its GPU's CTAs
+  // with a flag, (4) every CTA reads the global sums (exact integers: identical bits on every GPU).
+  // Ring invariants as in col_allreduce: CTA 0 zeroes slot cstep + 1 (local replicas and global)
+  // before arriving at this step's barriers; a peer adds into that slot only after this GPU's CTA 0
+  // arrived at this step's cross barrier.
+  template <typename Writer>
+  __device__ void col_allreduce_xgpu(int L1, double v, const double (&sc)[2], const double (&inv)[2], int64_t slot0,
+                                     int64_t off, Writer&& wr) {
+    unsigned long long* cur = colacc + off;
+    if (tid < L1) atomicAdd(cur, static_cast<unsigned long long>(__double2ll_rn(v * sc[tid < l ? 0 : 1])));
+    const int nslot = int((cstep + 1) % 3), cslot = int(cstep % 3);
+    auto gacc = [&](int p, int sl, int e) {
+      return reinterpret_cast<unsigned long long*>(a.peer_sync[p] + kSweepGaccOffset) +
+             (int64_t(sl) * kColAccMax + e) * kColAccSpacing;
+    };
+    if (g == 0 && tid < L1) {
+#pragma unroll
+      for (int rp = 0; rp < kColAccReps; ++rp)
+        colacc[((cstep + 1) % 3) * kColAccStride + (int64_t(rp) * kColAccMax + tid) * kColAccSpacing] = 0ull;
+      *gacc(a.rank, nslot, tid) = 0ull;
+    }
+    prof_tick(kPfOther);
+    barrier();
+    unsigned* flag = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(a.barrier) + kSweepFlagOffset);
+    if (g == 0) {
+      if (tid < L1) {
+        unsigned long long sum = 0ull;
+#pragma unroll
+        for (int rp = 0; rp < kColAccReps; ++rp)
+          sum += ld_cg(colacc + slot0 + (int64_t(rp) * kColAccMax + tid) * kColAccSpacing);
+        for (int p = 0; p < a.world; ++p) red_relaxed_sys_add_u64(gacc(p, cslot, tid), sum);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int p = 0; p < a.world; ++p)
+          red_release_sys_add(reinterpret_cast<unsigned*>(a.peer_sync[p] + kSweepXcolOffset), 1u);
+        const unsigned target = (cstep + 1) * unsigned(a.world);
+        while (ld_acquire_sys(reinterpret_cast<const unsigned*>(a.peer_sync[a.rank] + kSweepXcolOffset)) < target) {
+        }
+        st_release_gpu(flag, cstep + 1);
+      }
+      __syncthreads();
+    } else {
+      if (tid == 0)
+        while (ld_acquire_gpu(flag) < cstep + 1) {
+        }
+      __syncthreads();
+    }
+    prof_tick(kPfBarrier1);
+    if (tid < L1) {
+      const long long sum = static_cast<long long>(ld_cg(gacc(a.rank, cslot, tid)));
       wr(tid, double(sum) * inv[tid < l ? 0 : 1]);
     }
     ++cstep;
@@ -1569,15 +1633,17 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
 }
 
 template <typename T>
-int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream) {
+int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream, bool zero_sync) {
   if (plan.grid <= 0) throw CudaError("sweeps: problem does not fit the persistent kernel");
   const SmemLayout L =
       make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem, plan.qring);
-  RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, kSweepSyncBytes, stream));
+  if (zero_sync) RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, kSweepSyncBytes, stream));
   if (args.l + 1 > kColAccMax) throw CudaError("sweeps: sketch width above the column-reduction capacity");
   SweepArgs<T> a = args;
   // RNMF_COL_ORDERED: testing knob, column-step reduction through the ordered partial buffers
   if (std::getenv("RNMF_COL_ORDERED")) a.flags |= kColOrdered;
+  // RNMF_XGPU_FLAT: testing knob, the flat cross-GPU column step (every CTA adds into every GPU)
+  if (std::getenv("RNMF_XGPU_FLAT")) a.flags |= kXFlat;
   int64_t RM = plan.rows_per_cta, NCM = plan.cols_per_cta;
   void* kargs[] = {&a, const_cast<SmemLayout*>(&L), &RM, &NCM};
   const void* stream64 = nullptr;
@@ -1599,8 +1665,8 @@ int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t 
 
 template SweepPlan plan_sweeps<float>(int64_t, int64_t, int, int, int, int);
 template SweepPlan plan_sweeps<double>(int64_t, int64_t, int, int, int, int);
-template int launch_sweeps<float>(const SweepArgs<float>&, const SweepPlan&, cudaStream_t);
-template int launch_sweeps<double>(const SweepArgs<double>&, const SweepPlan&, cudaStream_t);
+template int launch_sweeps<float>(const SweepArgs<float>&, const SweepPlan&, cudaStream_t, bool);
+template int launch_sweeps<double>(const SweepArgs<double>&, const SweepPlan&, cudaStream_t, bool);
 
 bool sweep_prof_compiled() { return kSweepProf; }
 

@@ -893,6 +893,18 @@ struct LoopIO {
   bool init_wt;
 };
 
+// Row-sharded launches: zero this GPU's sync block, then an NCCL all-reduce, so that no GPU's
+// kernel can add into a peer's sync block before that peer has zeroed it for this launch.
+template <typename T>
+static int launch_sweeps_synced(rnmf_gpu_context* ctx, Engine<T>& eng, const SweepArgs<T>& a, const SweepPlan& plan,
+                                cudaStream_t st) {
+  if (!eng.sharded()) return launch_sweeps<T>(a, plan, st);
+  RNMF_CUDA(cudaMemsetAsync(ctx->sync_block, 0, kSweepSyncBytes, st));
+  double* tok = ctx->d<double>("sw.launch_token", 1);
+  eng.allreduce(tok, 1);
+  return launch_sweeps<T>(a, plan, st, false);
+}
+
 template <typename T>
 static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnmf_solver_options& o, LoopIO<T>& io,
                      std::chrono::steady_clock::time_point t0, double x_norm, rnmf_trace_record* trace,
@@ -1018,7 +1030,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
       a.t_begin = tb;
       a.t_end = t_end;
       if (fresh_order) a.order = dord + (tb - t_begin) * k;
-      tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, st); });
+      tm.span(kSweeps, [&] { tm.launches += launch_sweeps_synced<T>(ctx, eng, a, plan, st); });
       RNMF_CUDA(cudaMemcpyAsync(hstat, a.status, 3 * sizeof(long long), cudaMemcpyDeviceToHost, st));
       if (prof) RNMF_CUDA(cudaMemcpyAsync(hprof, a.prof, kSweepProfSlots * sizeof(long long), cudaMemcpyDeviceToHost, st));
       // Without reseed_dead the launch never hands control back mid-chunk, so the full-space metrics
@@ -1348,7 +1360,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
     const int64_t plen = sweep_part_len(l, k);
     a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
     a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
-    tm.span(kInit, [&] { tm.launches += launch_sweeps<T>(a, plan, ctx->stream); });
+    tm.span(kInit, [&] { tm.launches += launch_sweeps_synced<T>(ctx, eng, a, plan, ctx->stream); });
     eng.export_(q_out, location, q, size_t(m) * l);
     eng.export_(b_out, location, b, size_t(l) * n);
     if (wt_out) {
