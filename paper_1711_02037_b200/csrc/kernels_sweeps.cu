@@ -143,6 +143,7 @@ struct Sweeper {
   int qst = 0;  // stages
   int64_t qnch = 0, qissued = 0, qused = 0;
   unsigned xepoch = 0;         // cross-GPU barriers passed (row-sharded runs)
+  unsigned x2epoch = 0;        // hierarchical cross_allreduce calls (row-sharded runs)
   unsigned cur_t = 0;          // sweep being computed (reseed_dead liveness stamps)
   bool wpos = false;           // this thread lifted a positive W entry in the current column
   int xslot = 0;               // exchange-buffer slot of the next cross_allreduce
@@ -323,6 +324,43 @@ struct Sweeper {
   template <typename Get, typename Put>
   __device__ void cross_allreduce(int L, Get&& get, Put&& put) {
     if (!sharded()) return;
+    if (!(a.flags & kXFlat)) {
+      // hierarchical: a local grid barrier (every CTA here finished reading the slot the peers may
+      // rewrite next), CTA 0 writes and meets the other GPUs' CTA 0s, then releases this GPU's CTAs
+      barrier();
+      x2epoch += 1;
+      unsigned* flag2 = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned char*>(a.barrier) + kSweepFlagOffset + 64);
+      if (g == 0) {
+        for (int e = tid; e < L; e += kSwThreads) {
+          const double v = get(e);
+          for (int p = 0; p < a.world; ++p) xbuf(p, xslot, a.rank)[e] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int p = 0; p < a.world; ++p)
+            red_release_sys_add(reinterpret_cast<unsigned*>(a.peer_sync[p] + kSweepXcolOffset + 64), 1u);
+          const unsigned target = x2epoch * unsigned(a.world);
+          while (ld_acquire_sys(reinterpret_cast<const unsigned*>(a.peer_sync[a.rank] + kSweepXcolOffset + 64)) <
+                 target) {
+          }
+          st_release_gpu(flag2, x2epoch);
+        }
+        __syncthreads();
+      } else {
+        if (tid == 0)
+          while (ld_acquire_gpu(flag2) < x2epoch) {
+          }
+        __syncthreads();
+      }
+      for (int e = tid; e < L; e += kSwThreads) {
+        double s2 = 0.0;
+        for (int r = 0; r < a.world; ++r) s2 += __ldcg(xbuf(a.rank, xslot, r) + e);
+        put(e, s2);
+      }
+      xslot ^= 1;
+      __syncthreads();
+      return;
+    }
     if (g == 0)
       for (int e = tid; e < L; e += kSwThreads) {
         const double v = get(e);
