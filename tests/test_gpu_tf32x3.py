@@ -72,3 +72,20 @@ def test_tf32x3_rqb_projector(gpu, oracle):
     b = r.b.astype(np.float64)
     np.testing.assert_allclose(q.T @ q, np.eye(20), atol=1e-5)
     np.testing.assert_allclose(q @ b, qo @ bo, atol=2e-5 * np.abs(x).max())
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (5, 3, 2), (1000, 7, 3), (7, 1000, 3), (129, 33, 4), (64, 4000, 8)])
+def test_tf32x3_edge_shapes(gpu, oracle, m, n, k):
+    """Tiny and ragged shapes through the tensor-core sketch and metrics kernels (partial 128-row
+    tiles, fewer columns than one 32-wide stage, l clamped to min(m, n))."""
+    x = oracle.synth_lowrank(m, n, min(k, m, n), 0.1, 40 + m + n)
+    o = gpu.SolverOptions(rank=k, max_iter=8, tol=1e-300, oversampling=4, power_iterations=1, seed=2)
+    if k > min(m, n):
+        o.rank = min(m, n)
+    l = min(o.rank + 4, m, n)
+    om, w0, h0 = workloads.injected_inputs(5, m, n, o.rank, l)
+    ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    o.math_mode = gpu.MathMode.TF32x3
+    res = gpu.rhals_fit(x.astype(np.float32), o, omega=om, w0=w0, h0=h0)
+    assert len(res.trace) == len(ref.trace)
+    assert abs(res.trace[-1].rel_err - ref.trace[-1]["rel_err"]) <= 1e-4 + 1e-3 * ref.trace[-1]["rel_err"]
