@@ -19,3 +19,11 @@ for K in rhals_sweeps_kernel tc_xht_resid_kernel tc_xw_kernel tc_xtw_kernel; do
     -o $OUT/${K}_${CFG} python tools/run_fit.py --config $CFG --fits 1 > $OUT/ncu_${K}.log 2>&1
   echo "ncu $K rc=$?"
 done
+# other configs (bench lines) and the accuracy / streaming probes
+for C2 in C3 C4 C1; do
+  timeout 600 python bench.py --config $C2 --steps 3 --no-cpu-baseline > $OUT/bench_$C2.json 2> $OUT/bench_$C2.err
+  echo "bench $C2 rc=$?"
+done
+[ -x tools/sketch_acc ] && ./tools/sketch_acc 32256 2410 36 10 > $OUT/sketch_acc_c2.txt 2>&1
+timeout 600 python tools/bench_streaming.py > $OUT/streaming_c2.json 2>&1
+echo "streaming rc=$?"
