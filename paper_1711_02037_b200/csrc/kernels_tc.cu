@@ -961,6 +961,53 @@ __global__ void __launch_bounds__(kPgwThreads) tc_pgw_kernel(const float* __rest
   }
 }
 
+// All operand splits of one tensor-core metrics evaluation in one launch (regions of a flat index):
+//   [0, A)   H rows      -> st_hi / st_lo (npad x ldn): the S^T operand of X H^T
+//   [A, B)   W (m x k)   -> w_hi / w_lo (m x kw)      : A operand of the residual's W H
+//   [B, C)   H (k x n)   -> ht_hi / ht_lo (ldn x kw)  : B operand of the residual's W H
+//   [C, D)   W (m x k)   -> sw_hi / sw_lo (npad x ldm): the S^T operand of X^T W
+// hi = rna_tf32(v), lo = rna_tf32(v - hi) everywhere (as the separate prep kernels).
+__global__ void tc_metrics_prep_kernel(const float* __restrict__ w, const float* __restrict__ h, int64_t m, int64_t n,
+                                       int k, int npad, int kw, int64_t ldn, int64_t ldm, float* __restrict__ st_hi,
+                                       float* __restrict__ st_lo, float* __restrict__ w_hi, float* __restrict__ w_lo,
+                                       float* __restrict__ ht_hi, float* __restrict__ ht_lo, float* __restrict__ sw_hi,
+                                       float* __restrict__ sw_lo) {
+  const int64_t A = int64_t(npad) * ldn, B = A + m * kw, Cc = B + ldn * kw, D = Cc + int64_t(npad) * ldm;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < D; e += int64_t(gridDim.x) * blockDim.x) {
+    float v;
+    float *hi, *lo;
+    if (e < A) {
+      const int j = int(e / ldn);
+      const int64_t c = e % ldn;
+      v = (j < k && c < n) ? h[int64_t(j) * n + c] : 0.f;
+      hi = st_hi + e;
+      lo = st_lo + e;
+    } else if (e < B) {
+      const int64_t f = e - A, i = f / kw;
+      const int j = int(f % kw);
+      v = j < k ? w[i * k + j] : 0.f;
+      hi = w_hi + f;
+      lo = w_lo + f;
+    } else if (e < Cc) {
+      const int64_t f = e - B, c = f / kw;
+      const int j = int(f % kw);
+      v = (j < k && c < n) ? h[int64_t(j) * n + c] : 0.f;
+      hi = ht_hi + f;
+      lo = ht_lo + f;
+    } else {
+      const int64_t f = e - Cc;
+      const int j = int(f / ldm);
+      const int64_t i = f % ldm;
+      v = (j < k && i < m) ? w[i * k + j] : 0.f;
+      hi = sw_hi + f;
+      lo = sw_lo + f;
+    }
+    const float vh = tc::tf32_hi(v);
+    *hi = vh;
+    *lo = tc::tf32_hi(v - vh);
+  }
+}
+
 template <int KW>
 void tc_resid_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* w_hi, const float* w_lo,
                      const float* ht_hi, const float* ht_lo, double* part_obj, int grid, cudaStream_t stream) {
@@ -989,6 +1036,20 @@ int launch_tc_prep_rows(const float* src, int c, int64_t n, float* st_hi, float*
 }
 
 int tc_resid_kw(int k) { return k <= 32 ? 32 : 64; }
+
+int launch_tc_metrics_prep(const float* w, int64_t m, const float* h, int64_t n, int k, float* st_hi, float* st_lo,
+                           float* w_hi, float* w_lo, float* ht_hi, float* ht_lo, float* sw_hi, float* sw_lo,
+                           cudaStream_t stream) {
+  const int npad = tc_npad(k), kw = tc_resid_kw(k);
+  const int64_t ldn = tc_st_pitch(n), ldm = tc_st_pitch(m);
+  const int64_t total = int64_t(npad) * ldn + m * kw + ldn * kw + int64_t(npad) * ldm;
+  const int blocks = int(std::min<int64_t>(ceil_div(total, 256), 148 * 8));
+  tc_metrics_prep_kernel<<<blocks, 256, 0, stream>>>(w, h, m, n, k, npad, kw, ldn, ldm, st_hi, st_lo, w_hi, w_lo,
+                                                     ht_hi, ht_lo, sw_hi, sw_lo);
+  RNMF_CUDA_LAUNCH();
+  return 1;
+}
+
 
 int launch_tc_resid_prep(const float* w, int64_t m, const float* h, int64_t n, int k, float* w_hi, float* w_lo,
                          float* ht_hi, float* ht_lo, cudaStream_t stream) {

@@ -851,8 +851,7 @@ class Engine {
       allreduce(wtw, size_t(k) * k);  // W^T W over all rows (H H^T is replicated)
       // X H^T (m x k) -> projected grad_W partials
       int b1 = 0, b2 = 0, b0 = 0;
-      tm_.launches += launch_tc_prep_rows(h, k, n, sth, stl, st_);
-      tm_.launches += launch_tc_resid_prep(w, m, h, n, k, wh, wl, hth, htl, st_);
+      tm_.launches += launch_tc_metrics_prep(w, m, h, n, k, sth, stl, wh, wl, hth, htl, swh, swl, st_);
       if (fused) {  // X H^T and the residual in one X pass
         tm_.launches += launch_tc_xht_resid(x, m, n, ldx, sth, stl, wh, wl, hth, htl, k, xht, pobj, &b0, sms, st_);
       } else {
@@ -861,7 +860,6 @@ class Engine {
       }
       tm_.launches += launch_tc_pgw(xht, w, m, k, hht, ppgw, &b1, st_);
       // X^T W (n x k split partials) -> projected grad_H partials
-      tm_.launches += launch_tc_prep_st(w, m, k, swh, swl, st_);
       tm_.launches += launch_tc_xtw(x, m, n, ldx, swh, swl, k, part, splits, true, sms, st_);
       if (sharded()) {
         float* wtx1 = ctx_->d<float>("met.wtx1", size_t(n) * k);

@@ -35,6 +35,12 @@ int launch_tc_xht_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const
                         const float* w_hi, const float* w_lo, const float* ht_hi, const float* ht_lo, int k, float* xht,
                         double* part_obj, int* nblocks, int sm_count, cudaStream_t stream);
 
+// every operand split of one evaluation in one launch: launch_tc_prep_rows(H) + launch_tc_resid_prep
+// + launch_tc_prep_st(W) (sw_hi / sw_lo: tc_npad(k) x tc_st_pitch(m))
+int launch_tc_metrics_prep(const float* w, int64_t m, const float* h, int64_t n, int k, float* st_hi, float* st_lo,
+                           float* w_hi, float* w_lo, float* ht_hi, float* ht_lo, float* sw_hi, float* sw_lo,
+                           cudaStream_t stream);
+
 int launch_tc_pgw(const float* xht, const float* w, int64_t m, int k, const double* hht, double* part_pgw,
                   int* nblocks, cudaStream_t stream);
 int tc_pgw_blocks(int64_t m);
