@@ -544,24 +544,31 @@ __global__ void __launch_bounds__(kThreads) gram_cols_kernel(const T* __restrict
 // flight per thread), groups combined in fixed order (deterministic)
 __global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nparts, int len,
                                                            double* out) {
-  __shared__ double gs[4][64];
-  const int ei = threadIdx.x % 64, gi = threadIdx.x / 64;
-  const int e = blockIdx.x * 64 + ei;
-  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  // 32 entries x 8 part-slices per block; each slice keeps 8 independent loads in flight, the
+  // slices are combined in fixed order (deterministic)
+  __shared__ double gs[8][33];
+  const int ei = threadIdx.x % 32, gi = threadIdx.x / 32;
+  const int e = blockIdx.x * 32 + ei;
+  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (e < len) {
     int p = gi;
-    for (; p + 12 < nparts; p += 16) {
-      double v[4];
+    for (; p + 56 < nparts; p += 64) {
+      double v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = part[int64_t(p + 4 * u) * len + e];
+      for (int u = 0; u < 8; ++u) v[u] = part[int64_t(p + 8 * u) * len + e];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] += v[u];
+      for (int u = 0; u < 8; ++u) a[u] += v[u];
     }
-    for (; p < nparts; p += 4) a[0] += part[int64_t(p) * len + e];
+    for (; p < nparts; p += 8) a[0] += part[int64_t(p) * len + e];
   }
-  gs[gi][ei] = (a[0] + a[1]) + (a[2] + a[3]);
+  gs[gi][ei] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   __syncthreads();
-  if (gi == 0 && e < len) out[e] = ((gs[0][ei] + gs[1][ei]) + gs[2][ei]) + gs[3][ei];
+  if (gi == 0 && e < len) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += gs[q][ei];
+    out[e] = t;
+  }
 }
 
 template <typename T>
@@ -774,7 +781,7 @@ int launch_gram_rows(const T* a, int64_t rows, int c, double* part, double* g, c
   const size_t sm = size_t(kGramChunk) * c * sizeof(double);
   gram_rows_kernel<T><<<np, kThreads, sm, stream>>>(a, rows, c, part);
   RNMF_CUDA_LAUNCH();
-  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 64)), 256, 0, stream>>>(part, np, c * c, g);
+  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 32)), 256, 0, stream>>>(part, np, c * c, g);
   RNMF_CUDA_LAUNCH();
   return 2;
 }
@@ -786,7 +793,7 @@ int launch_gram_cols(const T* a, int c, int64_t cols, double* part, double* g, c
   const size_t sm = size_t(kGramChunk) * c * sizeof(double);
   gram_cols_kernel<T><<<np, kThreads, sm, stream>>>(a, c, cols, part);
   RNMF_CUDA_LAUNCH();
-  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 64)), 256, 0, stream>>>(part, np, c * c, g);
+  reduce_parts_kernel<<<unsigned(ceil_div(c * c, 32)), 256, 0, stream>>>(part, np, c * c, g);
   RNMF_CUDA_LAUNCH();
   return 2;
 }
@@ -816,7 +823,7 @@ int launch_widen(const T* in, int64_t count, double* out, cudaStream_t stream) {
 }
 
 int launch_reduce_parts(const double* part, int nparts, int len, double* out, cudaStream_t stream) {
-  reduce_parts_kernel<<<unsigned(ceil_div(len, 64)), 256, 0, stream>>>(part, nparts, len, out);
+  reduce_parts_kernel<<<unsigned(ceil_div(len, 32)), 256, 0, stream>>>(part, nparts, len, out);
   RNMF_CUDA_LAUNCH();
   return 1;
 }
