@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kCqThreads) cq_apply_kernel(const TIn* __restr
 }
 
 inline int gram_blocks(int64_t rows) {
-  return int(std::max<int64_t>(1, std::min<int64_t>(148, ceil_div(rows, 256))));
+  return int(std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(rows, 64))));
 }
 
 }  // namespace
