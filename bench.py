@@ -6,7 +6,13 @@ sweeps/s of whole fits with X resident in HBM (X larger than L2, so no flush is 
 is the same metric through the public API with X in pinned host memory (H2D of X and D2H of
 W, H and the trace inside every step).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+Default workload: BASELINE config C4 (200,000 x 20,000, rank 40 + noise, fp32, k 40, p 20, q 2,
+200 sweeps), the largest config that fits one GPU and the one BASELINE.md names for the 1 -> 8
+GPU curve.  C1-C3 are selectable (--config), C5 runs in full at >= 4 GPUs and on labelled row
+slices below that (slice_rows).  C4 / C5 X is generated on the device per shard (seeded per
+row block, shard-count independent: workloads.noisy_lowrank_shard).
 
 N > 1 (torchrun, one process per GPU): ONE fit of the config with X sharded by rows over the N
 GPUs (paper_1711_02037_b200.distributed; strong scaling); `value` = sweeps/s of that fit, device
@@ -106,97 +112,147 @@ def load_traffic(cfg_name: str):
         return None
 
 
-def make_workload(cfg_name: str, device):
-    """X (device, fp32/fp64), injected Omega / unscaled init draws, solver options."""
+def slice_rows(cfg_name: str, world: int):
+    """Rows of the config a `world`-GPU run factorises.  C5 (200 GB fp32) does not fit one GPU:
+    BASELINE.json runs it at 8 and 4 GPUs in full and at 2 GPUs on a 100,000-row slice; a single
+    GPU takes a 40,000-row slice (16 GB) -- both labelled in `config`."""
+    cfg = workloads.CONFIGS[cfg_name]
+    if cfg_name == "C5" and world < 4:
+        return 100000 if world >= 2 else 40000
+    return cfg.m
+
+
+def host_matrix(cfg_name: str):
+    if cfg_name == "C1":
+        return workloads.c1_matrix(0)
+    if cfg_name == "C2":
+        return workloads.faces_matrix(0)
+    if cfg_name == "C3":
+        return workloads.unmixing_matrix(0)
+    return None
+
+
+def make_workload(cfg_name: str, device, world: int = 1, rank: int = 0, sharded: bool = False):
+    """This rank's X rows on the device (C4/C5: generated per shard by the seeded per-block
+    generator, no rank builds the whole matrix), the injected Omega / unscaled init draws (this
+    rank's W0 rows), the solver options and (row offset, rows, total rows)."""
     import torch
 
     from paper_1711_02037_b200 import api
 
     cfg = workloads.CONFIGS[cfg_name]
-    if cfg_name == "C1":
-        x = workloads.c1_matrix(0)
-    elif cfg_name == "C2":
-        x = workloads.faces_matrix(0)
-    elif cfg_name == "C3":
-        x = workloads.unmixing_matrix(0)
-    elif cfg_name == "C4":
-        x = None
+    m_total = slice_rows(cfg_name, world)
+    if world > 1 or sharded:
+        from paper_1711_02037_b200 import distributed as pdist
+
+        off, cnt = pdist.shard_rows(m_total, world, rank)
     else:
-        raise SystemExit(f"config {cfg_name} is multi-GPU only (200 GB); not runnable in this build")
+        off, cnt = 0, m_total
+    x = host_matrix(cfg_name)
     if x is None:
-        xd = workloads.noisy_lowrank_device(0, cfg.m, cfg.n, 40, 0.5, 0.1, device=device)
+        xd = workloads.config_shard(cfg_name, off, cnt, device=device)
     else:
-        xd = torch.from_numpy(x).to(device)
-    l = min(cfg.k + cfg.p, cfg.m, cfg.n)
-    omega, w0, h0 = workloads.injected_inputs(0, cfg.m, cfg.n, cfg.k, l)
+        xd = torch.from_numpy(np.ascontiguousarray(x[off:off + cnt])).to(device)
+    l = min(cfg.k + cfg.p, m_total, cfg.n)
+    omega, w0, h0 = workloads.injected_inputs(0, m_total, cfg.n, cfg.k, l)
+    w0 = np.ascontiguousarray(w0[off:off + cnt])
     opts = api.SolverOptions(rank=cfg.k, oversampling=cfg.p, power_iterations=cfg.q, max_iter=cfg.iters,
                              tol=1e-300, seed=0)
-    return cfg, xd, omega, w0, h0, opts
+    return cfg, xd, omega, w0, h0, opts, (off, cnt, m_total)
 
 
-def cpu_baseline(cfg_name: str, x_host: np.ndarray, cfg, omega, w0, h0, threads: int = 1):
-    """Oracle (fp64 C++ restatement of the reference) on the box's host cores: sketch + 10 sweeps
-    measured (trace_full_every = 10 makes that exactly one sweep/metrics period), extrapolated to
-    the config's full sweep count: t(0) + (iters/10) * (t(10) - t(0))."""
+# ---- CPU baseline: the fp64 oracle (restatement of the reference rhals_fit) on host cores --------
+# C1-C3: the whole fit is timed (every sweep).  C4 / C5 need ~100 GB / ~1.2 TB of fp64 reference
+# temporaries (the m x n residual of p/src/rhals.cpp:141): the oracle runs on row slices of the
+# config (full n, k, l, q; the same per-block generator) at two heights m1 < m2, each with 0 and
+# 10 sweeps (10 sweeps = one full-space metrics period), and the full fit is extrapolated with
+# t(m, s) = A(m) + (s / 10) P(m), A and P linear in m (sketch / metrics / W-phase work is linear
+# in m at fixed n; the H phase is independent of m).  Labelled "extrapolated".
+SLICE_ROWS = {"C4": (1000, 3000), "C5": (250, 750)}
+
+
+def _oracle_fit_s(orc, x64, cfg, omega, w0, h0, sweeps):
+    base = dict(rank=cfg.k, tol=1e-300, oversampling=cfg.p, power_iterations=cfg.q, seed=0, trace_full_every=10,
+                max_iter=sweeps)
+    t = time.perf_counter()
+    orc.rhals_fit(x64, base, omega=omega, w0=w0, h0=h0)
+    return time.perf_counter() - t
+
+
+def cpu_sample(cfg_name: str, threads: int, x_host=None, m_full=None):
+    """One bounded CPU sample of the config -> dict(value iters/s of the full config, est_fit_s,
+    wall_s actually spent, sample description, extrapolated flag)."""
     from oracle import oracle as orc
 
     orc.set_threads(threads)
-    x64 = np.ascontiguousarray(x_host, dtype=np.float64)
-    base = dict(rank=cfg.k, tol=1e-300, oversampling=cfg.p, power_iterations=cfg.q, seed=0, trace_full_every=10)
-    t = time.perf_counter()
-    orc.rhals_fit(x64, dict(base, max_iter=0), omega=omega, w0=w0, h0=h0)
-    t0 = time.perf_counter() - t
-    t = time.perf_counter()
-    orc.rhals_fit(x64, dict(base, max_iter=10), omega=omega, w0=w0, h0=h0)
-    t10 = time.perf_counter() - t
-    est = t0 + (cfg.iters / 10.0) * max(t10 - t0, 0.0)
-    return {
-        "value": cfg.iters / est,
-        "unit": "iters/s",
-        "cores": threads,
-        "kind": "port",
-        "sample": f"{cfg_name} full matrix, fp64 oracle: rhals_fit with 0 and 10 sweeps measured "
-                  f"({t0:.2f}s, {t10:.2f}s), extrapolated to {cfg.iters} sweeps = {est:.2f}s",
-        "est_fit_s": est,
-    }
+    cfg = workloads.CONFIGS[cfg_name]
+    t_all = time.perf_counter()
+    if cfg_name in SLICE_ROWS:
+        import torch
+
+        m_full = cfg.m if m_full is None else m_full
+        pts = {}
+        for ms in SLICE_ROWS[cfg_name]:
+            dev = "cuda" if torch.cuda.is_available() else "cpu"  # the bench's own rows 0..ms-1 on a GPU box
+            x64 = workloads.config_shard(cfg_name, 0, ms, device=dev).cpu().numpy().astype(np.float64)
+            l = min(cfg.k + cfg.p, ms, cfg.n)
+            om, w0, h0 = workloads.injected_inputs(0, ms, cfg.n, cfg.k, l)
+            pts[ms] = (_oracle_fit_s(orc, x64, cfg, om, w0, h0, 0), _oracle_fit_s(orc, x64, cfg, om, w0, h0, 10))
+            del x64
+            torch.cuda.empty_cache() if torch.cuda.is_available() else None
+        (m1, m2) = SLICE_ROWS[cfg_name]
+        a_slope = (pts[m2][0] - pts[m1][0]) / (m2 - m1)
+        p_slope = ((pts[m2][1] - pts[m2][0]) - (pts[m1][1] - pts[m1][0])) / (m2 - m1)
+        a_full = pts[m1][0] + a_slope * (m_full - m1)
+        p_full = (pts[m1][1] - pts[m1][0]) + p_slope * (m_full - m1)
+        est = a_full + (cfg.iters / 10.0) * max(p_full, 0.0)
+        sample = (f"{cfg_name} row slices m={m1},{m2} (full n={cfg.n}, k={cfg.k}, l={cfg.k + cfg.p}, q={cfg.q}), "
+                  f"fp64 oracle with 0 / 10 sweeps: " +
+                  ", ".join(f"m={ms}: {t0:.2f}s / {t10:.2f}s" for ms, (t0, t10) in pts.items()) +
+                  f"; extrapolated to {m_full} rows x {cfg.iters} sweeps = {est:.1f}s")
+        extrap = True
+    else:
+        x = host_matrix(cfg_name) if x_host is None else x_host
+        x64 = np.ascontiguousarray(x, dtype=np.float64)
+        l = min(cfg.k + cfg.p, cfg.m, cfg.n)
+        om, w0, h0 = workloads.injected_inputs(0, cfg.m, cfg.n, cfg.k, l)
+        est = _oracle_fit_s(orc, x64, cfg, om, w0, h0, cfg.iters)
+        sample = f"{cfg_name} full matrix, fp64 oracle rhals_fit, all {cfg.iters} sweeps timed ({est:.2f}s)"
+        extrap = False
+    return {"value": cfg.iters / est, "unit": "iters/s", "cores": threads, "kind": "port", "sample": sample,
+            "est_fit_s": est, "wall_s": time.perf_counter() - t_all, "extrapolated": extrap}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU implementation (the oracle port; the
-    reference itself cannot be compiled here, no Eigen) on all host threads."""
+    """--impl reference: the reference algorithm's CPU implementation (the fp64 oracle port; the
+    reference itself cannot be compiled here: no Eigen) on all host threads, on this arm's config.
+    Each step is one bounded sample (C1-C3: one whole fit; C4/C5: the row-slice samples above)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = workloads.CONFIGS[args.config]
-    if args.config == "C1":
-        x = workloads.c1_matrix(0)
-    elif args.config == "C2":
-        x = workloads.faces_matrix(0)
-    elif args.config == "C3":
-        x = workloads.unmixing_matrix(0)
-    else:
-        print(json.dumps({"impl": "reference", "unavailable": f"{args.config} does not fit host-side fp64 oracle"}))
-        return
-    l = min(cfg.k + cfg.p, cfg.m, cfg.n)
-    omega, w0, h0 = workloads.injected_inputs(0, cfg.m, cfg.n, cfg.k, l)
     threads = os.cpu_count() or 1
+    x = host_matrix(args.config)
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args.config, x, cfg, omega, w0, h0, threads=threads)
+        r = cpu_sample(args.config, threads, x, m_full=slice_rows(args.config, args.gpus))
         if i >= args.warmup:
             vals.append(r)
-        if i + 1 >= args.warmup and len(vals) >= args.steps:
-            break
     v = float(np.mean([r["value"] for r in vals]))
     est = float(np.mean([r["est_fit_s"] for r in vals]))
+    wall = float(np.mean([r["wall_s"] for r in vals]))
+    m_total = slice_rows(args.config, args.gpus)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup,
+        # wall time of one measured sample; the full-config fit time it implies is est_fit_s
+        "ms_per_step": wall * 1e3, "est_fit_s": est, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "k": cfg.k, "p": cfg.p, "q": cfg.q,
-                   "iters": cfg.iters},
+        "config": {"workload": cfg.name + (f" rows 0..{m_total - 1}" if m_total != cfg.m else ""), "m": m_total,
+                   "n": cfg.n, "k": cfg.k, "p": cfg.p, "q": cfg.q, "iters": cfg.iters, "tol": 1e-300,
+                   "math_mode": "fp64 (CPU)", "parallelism": f"{threads} host threads"},
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": threads, "kind": "port",
-                         "sample": vals[0]["sample"] if vals else ""},
+                         "sample": vals[0]["sample"] if vals else "", "extrapolated": vals[0]["extrapolated"]},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -207,7 +263,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    # C4 (200,000 x 20,000, k 40, 200 sweeps, 16 GB fp32): the largest BASELINE config that fits one
+    # GPU and the config BASELINE.md names for the 1 -> 8 GPU curve
+    ap.add_argument("--config", default="C4", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # tf32x3: the X-streaming sketch GEMMs on tcgen05 tensor cores (3xTF32 split, chunked TMEM
@@ -234,18 +292,14 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
 
-    cfg, xd, omega, w0, h0, opts = make_workload(args.config, device)
+    cfg, xd, omega, w0, h0, opts, (off, cnt, m_total) = make_workload(args.config, device, world, rank, args.sharded)
     opts.math_mode = {"exact": api.MathMode.Exact, "tf32x3": api.MathMode.TF32x3, "tf32": api.MathMode.TF32}[args.math]
     esz = xd.element_size()
-    m_total = cfg.m
     if world > 1 or args.sharded:
         from paper_1711_02037_b200 import distributed as pdist
 
         ctx = (pdist.ShardedContext(local) if world > 1 else
                pdist.ShardedContext(local, rank=0, world=1, comm_id=pdist.comm_unique_id()))
-        off, cnt = pdist.shard_rows(m_total, world, rank)
-        xd = xd[off:off + cnt].contiguous()
-        w0 = np.ascontiguousarray(w0[off:off + cnt])
 
         def fit(x):
             return pdist.rhals_fit_sharded(x, opts, row_offset=off, m_total=m_total, ctx=ctx, omega=omega, w0=w0,
@@ -316,10 +370,10 @@ def main():
         e2e_total = float(t.item())
     e2e_value = sweeps * args.steps / (e2e_total / 1e3)
     m, n, k = xd.shape[0], cfg.n, cfg.k
-    l = min(cfg.k + cfg.p, m, n)
+    l = min(cfg.k + cfg.p, m_total, n)
     # whole job: every rank copies its X rows and W0 rows, Omega / H0 replicated; W rows + H back
-    h2d = cfg.m * n * esz + 8 * cfg.m * k + world * 8 * (n * l + k * n)
-    d2h = esz * (cfg.m * k + world * k * n) + world * 56 * (sweeps + 1)
+    h2d = m_total * n * esz + 8 * m_total * k + world * 8 * (n * l + k * n)
+    d2h = esz * (m_total * k + world * k * n) + world * 56 * (sweeps + 1)
 
     # the other sketch arithmetic (FFMA when the timed run used the tensor cores, and vice versa):
     # the same X passes once more for a second sketch roofline, outside the timed region
@@ -373,9 +427,11 @@ def main():
         "vs_baseline": None,
         "dtype": "f32" if esz == 4 else "f64",
         "data": "synthetic (seeded stand-in for the paper's dataset; see paper_1711_02037_b200/workloads.py)",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": n, "k": k, "p": cfg.p, "q": cfg.q, "iters": cfg.iters,
+        "config": {"workload": cfg.name + (f" rows 0..{m_total - 1} (slice)" if m_total != cfg.m else ""),
+                   "m": m_total, "n": n, "k": k, "p": cfg.p, "q": cfg.q, "iters": cfg.iters,
                    "tol": 1e-300, "math_mode": args.math,
-                   "parallelism": f"rows{world}" if world > 1 else "single-gpu",
+                   "parallelism": (f"rows{world}" if world > 1 else
+                                   "single-gpu, row-sharded code path (world 1)" if args.sharded else "single-gpu"),
                    "l2": (f"X per GPU = {m * n * esz / 1e6:.0f} MB > 126 MB L2 (no flush needed)" if flush is None
                           else f"X per GPU = {m * n * esz / 1e6:.0f} MB: L2 flushed (256 MB write) between steps")},
         "end_to_end_s": ms_per_step / 1e3,
@@ -416,8 +472,8 @@ def main():
     }
     if not args.no_cpu_baseline and world == 1:
         try:
-            x_host = xd.cpu().numpy()
-            line["cpu_baseline"] = cpu_baseline(args.config, x_host, cfg, omega, w0, h0, threads=1)
+            del x_pin, x_np
+            line["cpu_baseline"] = cpu_sample(args.config, os.cpu_count() or 1, m_full=m_total)
         except Exception as exc:  # reported, never silently dropped
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     print(json.dumps(line))

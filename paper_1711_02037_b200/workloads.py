@@ -91,27 +91,65 @@ def noisy_lowrank_matrix(seed: int, m: int, n: int, rank: int, sparsity: float, 
     return np.ascontiguousarray(x.astype(dtype))
 
 
-def noisy_lowrank_device(seed: int, m: int, n: int, rank: int, sparsity: float, noise_frac: float,
-                         device="cuda", row_block: int = 8192):
-    """Device generator for the multi-GB configs (C4/C5): same distribution as
-    noisy_lowrank_matrix, built block-row by block-row with torch on the GPU (fp32)."""
+GEN_BLOCK_ROWS = 4096
+
+
+def lowrank_expected_mean(rank: int, sparsity: float) -> float:
+    """E[(W0 H0)_ij] for W0, H0 = |N(0,1)| with a Bernoulli(sparsity) zero mask:
+    rank * (1 - sparsity)^2 * E|N(0,1)|^2 = rank * (1 - sparsity)^2 * 2 / pi."""
+    return rank * (1.0 - sparsity) ** 2 * 2.0 / np.pi
+
+
+def noisy_lowrank_shard(seed: int, m: int, n: int, rank: int, sparsity: float, noise_frac: float, row0: int,
+                        rows: int, device="cuda", block: int = GEN_BLOCK_ROWS):
+    """Rows [row0, row0 + rows) of the m x n C4/C5 matrix X = W0 H0 + |N(0, noise_frac * mean)|, generated
+    on the device without materialising any other rows (counter-based, keyed by
+    (seed, global row block), so every shard count produces the same global X).
+
+    * H0 (rank x n) = |N(0,1)| * Bernoulli mask from a generator keyed by the seed alone
+      (replicated on every rank);
+    * global row block b (rows [b*block, (b+1)*block)) draws its W0 rows and its noise from a
+      generator keyed by (seed, b);
+    * the noise scale uses the expected mean of W0 H0 (lowrank_expected_mean), which needs no
+      pass over the whole matrix.
+    fp32 on `device`; the GEMM W0_rows H0 runs in fp32 (TF32 off)."""
     import torch
 
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    w0 = torch.randn((m, rank), generator=g, device=device).abs_()
-    w0 *= (torch.rand((m, rank), generator=g, device=device) >= sparsity)
-    h0 = torch.randn((rank, n), generator=g, device=device).abs_()
-    h0 *= (torch.rand((rank, n), generator=g, device=device) >= sparsity)
-    # mean(W0 H0) = mean over rows of W0 times column sums of H0
-    mean = float((w0.sum(0) @ h0.sum(1)) / (m * n))
-    x = torch.empty((m, n), dtype=torch.float32, device=device)
-    for r0 in range(0, m, row_block):
-        r1 = min(m, r0 + row_block)
-        blk = w0[r0:r1] @ h0
-        blk += torch.randn(blk.shape, generator=g, device=device).abs_() * (noise_frac * mean)
-        x[r0:r1] = blk
+    if not (0 <= row0 and rows >= 0 and row0 + rows <= m):
+        raise ValueError(f"rows [{row0}, {row0 + rows}) outside 0..{m}")
+    dev = torch.device(device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(seed) * 1000003 + 17)
+    h0 = torch.randn((rank, n), generator=g, device=dev).abs_()
+    h0 *= (torch.rand((rank, n), generator=g, device=dev) >= sparsity)
+    sigma = noise_frac * lowrank_expected_mean(rank, sparsity)
+    x = torch.empty((rows, n), dtype=torch.float32, device=dev)
+    tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        for b in range(row0 // block, (row0 + rows + block - 1) // block if rows else row0 // block):
+            b0, b1 = b * block, min(m, (b + 1) * block)
+            g.manual_seed((int(seed) * 0x9E3779B1 + 0x632BE5AB * (b + 1)) & 0x7FFFFFFFFFFFFFFF)
+            w = torch.randn((b1 - b0, rank), generator=g, device=dev).abs_()
+            w *= (torch.rand((b1 - b0, rank), generator=g, device=dev) >= sparsity)
+            lo, hi = max(b0, row0), min(b1, row0 + rows)
+            blk = w[lo - b0:hi - b0] @ h0
+            noise = torch.randn((b1 - b0, n), generator=g, device=dev)[lo - b0:hi - b0]
+            blk += noise.abs_() * sigma
+            x[lo - row0:hi - row0] = blk
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = tf32
     return x
+
+
+def config_shard(cfg_name: str, row0: int, rows: int, device="cuda"):
+    """Device rows of a C4 / C5 workload (the seeded per-block generator above)."""
+    cfg = CONFIGS[cfg_name]
+    if cfg_name == "C4":
+        return noisy_lowrank_shard(0, cfg.m, cfg.n, 40, 0.5, 0.1, row0, rows, device)
+    if cfg_name == "C5":
+        return noisy_lowrank_shard(0, cfg.m, cfg.n, 64, 0.7, 0.05, row0, rows, device)
+    raise KeyError(cfg_name)
 
 
 def injected_inputs(seed: int, m: int, n: int, k: int, l: int, gaussian_omega: bool = True):

@@ -12,7 +12,9 @@ import pytest
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 FIELDS = ["iter", "objective", "rel_err", "pgrad", "pgrad_full", "objective_compressed"]
-CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "*.npz")))
+# config_*.npz are the full-size config traces of tests/test_gpu_configs.py (no X stored)
+CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "*.npz"))
+               if not os.path.basename(p).startswith("config_"))
 
 
 def load(name):

@@ -7,7 +7,7 @@
 set -u
 OUT=gpurun_out/prof
 mkdir -p $OUT
-CFG=${CFG:-C2}
+CFG=${CFG:-C4}
 timeout 900 python bench.py --config $CFG > $OUT/bench.json 2> $OUT/bench.err || { echo "bench failed"; tail $OUT/bench.err; exit 1; }
 timeout 900 python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline > $OUT/bench_short.json 2>&1 || { echo "short bench failed"; exit 1; }
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--fits", type=int, default=1)
     ap.add_argument("--iters", type=int, default=0, help="override sweep count")
     ap.add_argument("--math", default="tf32x3")
@@ -21,7 +21,7 @@ def main():
     import bench
     from paper_1711_02037_b200 import api
 
-    cfg, xd, omega, w0, h0, opts = bench.make_workload(args.config, torch.device("cuda", 0))
+    cfg, xd, omega, w0, h0, opts, _ = bench.make_workload(args.config, torch.device("cuda", 0))
     if args.iters:
         opts.max_iter = args.iters
     opts.math_mode = {"exact": api.MathMode.Exact, "tf32x3": api.MathMode.TF32x3, "tf32": api.MathMode.TF32}[args.math]
