@@ -244,7 +244,14 @@ struct SweepArgs {
   long long* prof;         // optional: per-phase cycle counters of CTA 0 (kSweepProfSlots)
   const int* order;        // Interleaved / Shuffled: component order, k per sweep of t_begin..t_end
                            // (nullptr: Grouped)
+  // fp32 streamed-Q path (SweepPlan::f32s): Q re-laid out as float4 columns, q4[i4 * m + r] =
+  // Q(r, 4 i4 .. 4 i4 + 3) (zero past l; sweep_relayout_q), and a k x m column-major W scratch the
+  // launch works in (W is transposed in at the start of the launch and back at the end)
+  const float* q4;
+  float* wc;
 };
+// q4 (ceil(l_pad / 4) float4 columns of m rows) from row-major Q (m x l); l_pad = SweepPlan::lreg
+int sweep_relayout_q(const float* q, int64_t m, int l, int l_pad, float* q4, cudaStream_t stream);
 bool sweep_prof_compiled();  // built with RNMF_SWEEP_PROF=1
 constexpr int kSweepProfSlots = 17;  // 16 buckets + barrier count
 
@@ -263,6 +270,8 @@ struct SweepPlan {
   int64_t cols_per_cta = 0;
   int lreg = 0;  // > 0: Q rows register-resident (rows_per_cta <= 256, l + 1 <= lreg <= 64)
   int qring = 0;  // > 0: streamed slabs through a shared-memory bulk-copy ring of that many stages
+  bool f32s = false;  // fp32 X, Q slab not resident: coalesced float4-column Q (SweepArgs::q4), fp32
+                      // FMA lift / recompress, column-major W scratch (SweepArgs::wc); lreg = padded l
 };
 template <typename T>
 SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem);

@@ -60,11 +60,13 @@ struct SmemLayout {
   size_t qs, wst, wcold, bc, hc, rc, total;
   // streamed Q slabs through a 2-stage bulk-copy ring (0: not used): stage = kSwThreads rows
   size_t qring, qring_stage, qbars, qring_n;
+  // fp32 streamed path: colnew as fp32 (lp floats, zero past l), E as fp32 (l x k) for grad_W
+  size_t cnf, ef;
 };
 
 constexpr int kQRingMax = 6;  // bulk-copy ring stages (fewer when shared memory is short)
 template <typename T>
-SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring = 0) {
+SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring = 0, int f32s_lp = 0) {
   SmemLayout L{};
   size_t d = 0;
   auto take = [&](size_t count) {  // 16-byte aligned (double2 loads)
@@ -99,11 +101,16 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring 
     return off;
   };
   L.qs = qs ? takeD(size_t(RM) * (l + 1)) : 0;
-  L.wcold = ring ? 0 : takeD(size_t(RM));  // the ring path keeps the lifted column in registers
+  // the ring and fp32 streamed paths keep the lifted column in registers
+  L.wcold = (ring || f32s_lp) ? 0 : takeD(size_t(RM));
   L.wst = qs ? takeT(size_t(k) * RM) : 0;
   L.bc = takeT(size_t(l) * ncp);
   L.hc = takeT(size_t(k) * ncp);
   L.rc = takeT(size_t(l) * ncp);
+  if (f32s_lp) {
+    L.cnf = takeT(size_t(f32s_lp));
+    L.ef = takeT(size_t(l) * ((k + 7) & ~7));
+  }
   if (ring) {
     b = (b + 127) / 128 * 128;
     L.qring_stage = size_t(kSwThreads) * l * sizeof(T);
@@ -125,6 +132,9 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring 
 // accumulation happen on the row while it is in registers (one pass over the slab per column).
 template <typename T, bool QS, int LREG>
 struct Sweeper {
+  // fp32 X with the Q slab not resident on chip: coalesced float4-column Q (a.q4), fp32 FMA lift and
+  // recompress (no fp64 conversions on the row stream), column-major W scratch (a.wc)
+  static constexpr bool F32S = !QS && LREG > 0 && sizeof(T) == 4;
   const SweepArgs<T>& a;
   int G, g, tid, lane, wid, l, k;
   int64_t r0, R, c0, NC, RM;
@@ -132,6 +142,7 @@ struct Sweeper {
   double *Wt, *Tm, *Em, *Vm, *Sm, *wn, *Pm, *colold, *colnew, *invd, *rdw, *red, *scal;
   double *Qs, *wcold;
   T *WsT, *Bc, *Hc, *Rc;
+  float *cnf = nullptr, *ef = nullptr;
   unsigned epoch = 0;
   int slot = 0;
   unsigned long long* colacc;  // fixed-point column accumulators (3-slot ring)
@@ -201,6 +212,10 @@ struct Sweeper {
     Bc = reinterpret_cast<T*>(smem + L.bc);
     Hc = reinterpret_cast<T*>(smem + L.hc);
     Rc = reinterpret_cast<T*>(smem + L.rc);
+    if (L.cnf) {
+      cnf = reinterpret_cast<float*>(smem + L.cnf);
+      ef = reinterpret_cast<float*>(smem + L.ef);
+    }
     colacc = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(a.barrier) + 128);
     if (L.qring) {
       qring = reinterpret_cast<const T*>(smem + L.qring);
@@ -614,6 +629,15 @@ struct Sweeper {
   // ---------------------------------------------------------------------------------------------
   __device__ void load_resident() {
     for (int i = tid; i < 64; i += kSwThreads) colnew[i] = 0.0;  // the padded tail stays zero
+    if constexpr (F32S) {
+      for (int i = tid; i < LREG; i += kSwThreads) cnf[i] = 0.f;
+      // W rows of this CTA into the column-major scratch (the launch works column by column)
+      for (int64_t e = tid; e < R * k; e += kSwThreads) {
+        const int64_t r = e / k;
+        const int j = int(e % k);
+        a.wc[int64_t(j) * a.m + r0 + r] = float(a.w[(r0 + r) * k + j]);
+      }
+    }
     if constexpr (QS) {
       for (int64_t e = tid; e < R * l; e += kSwThreads) {
         const int64_t r = e / l;
@@ -652,6 +676,14 @@ struct Sweeper {
   }
 
   __device__ void store_back(int64_t last, int stopped) {
+    if constexpr (F32S) {
+      if ((a.flags & kDoW) || a.order != nullptr)
+        for (int64_t e = tid; e < R * k; e += kSwThreads) {
+          const int64_t r = e / k;
+          const int j = int(e % k);
+          a.w[(r0 + r) * k + j] = T(a.wc[int64_t(j) * a.m + r0 + r]);
+        }
+    }
     if constexpr (QS) {
       for (int64_t e = tid; e < R * k; e += kSwThreads) {
         const int64_t r = e / k;
@@ -805,6 +837,7 @@ struct Sweeper {
         nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) * rden;
         colold[tid] = cur;
         colnew[tid] = nw;
+        if constexpr (F32S) cnf[tid] = float(nw);
       }
       const double sq = warp_allreduce_sum(nw * nw);
       if (lane == 0) scal[4 + wid] = sq;
@@ -890,6 +923,96 @@ struct Sweeper {
           }
 #pragma unroll
           for (int off = 8; off >= 1; off >>= 1) {
+            const bool hi = (lane & off) != 0;
+#pragma unroll
+            for (int e = 0; e < off; ++e) {
+              const double send = hi ? v[e] : v[e + off];
+              const double mine = hi ? v[e + off] : v[e];
+              v[e] = mine + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+          const int i = chunk * 32 + lane;
+          if (i < L1) red[wid * kRedStride + i] = v[0];
+        }
+      }
+    } else if constexpr (F32S) {
+      // fp32 streamed rows: thread t takes rows t, t + 256, ...; the row's float4 columns are
+      // coalesced 512-byte warp loads from a.q4; lift u = Q(r,:) colnew and the recompress partials
+      // Q(r,:)^T w, ||w||^2 in fp32 FMA (per-thread partials over a few rows), then the warp
+      // reduce-scatter switches to fp64 after two levels (partials over <= 4 threads' rows in fp32)
+      constexpr int L4 = LREG / 4;
+      constexpr int UNR = LREG <= 32 ? 2 : 1;
+      float acc[LREG];
+      float accn = 0.f;
+#pragma unroll
+      for (int i = 0; i < LREG; ++i) acc[i] = 0.f;
+      const float shiftf = float(shift);
+      const float4* q4 = reinterpret_cast<const float4*>(a.q4);
+      const float4* c4 = reinterpret_cast<const float4*>(cnf);
+      float* wcol = a.wc + int64_t(j) * a.m + r0;
+      for (int64_t rb = tid; rb < R; rb += int64_t(kSwThreads) * UNR) {
+        float4 qv[UNR][L4];
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int64_t r = rb + int64_t(kSwThreads) * uu;
+          const int64_t rr = r < R ? r0 + r : r0;  // clamped: in-range address, result unused
+#pragma unroll
+          for (int i4 = 0; i4 < L4; ++i4) qv[uu][i4] = __ldg(q4 + int64_t(i4) * a.m + rr);
+        }
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int64_t r = rb + int64_t(kSwThreads) * uu;
+          if (r >= R) continue;
+          float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;
+#pragma unroll
+          for (int i4 = 0; i4 < L4; ++i4) {
+            const float4 c = c4[i4];
+            u0 = fmaf(qv[uu][i4].x, c.x, u0);
+            u1 = fmaf(qv[uu][i4].y, c.y, u1);
+            u2 = fmaf(qv[uu][i4].z, c.z, u2);
+            u3 = fmaf(qv[uu][i4].w, c.w, u3);
+          }
+          float uf = (u0 + u1) + (u2 + u3);
+          if (beta != 0.0) uf -= shiftf;
+          const float wd = fmaxf(uf, 0.f);
+          wpos |= wd > 0.f;
+          wcol[r] = wd;
+#pragma unroll
+          for (int i4 = 0; i4 < L4; ++i4) {
+            acc[4 * i4] = fmaf(qv[uu][i4].x, wd, acc[4 * i4]);
+            acc[4 * i4 + 1] = fmaf(qv[uu][i4].y, wd, acc[4 * i4 + 1]);
+            acc[4 * i4 + 2] = fmaf(qv[uu][i4].z, wd, acc[4 * i4 + 2]);
+            acc[4 * i4 + 3] = fmaf(qv[uu][i4].w, wd, acc[4 * i4 + 3]);
+          }
+          accn = fmaf(wd, wd, accn);
+        }
+      }
+      prof_tick(kPfLift);
+#pragma unroll
+      for (int chunk = 0; chunk < (LREG + 32) / 32; ++chunk) {
+        if (chunk * 32 < L1) {
+          // entry i of this thread's vector: acc[i] (i < l; zero for l <= i < LREG), accn at i = l
+          auto val = [&](int i) -> float {
+            return (i < LREG ? acc[i < LREG ? i : 0] : 0.f) + (i == l ? accn : 0.f);
+          };
+          float v16[16];
+          {
+            const bool hi = (lane & 16) != 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float va = val(chunk * 32 + e), vb = val(chunk * 32 + e + 16);
+              v16[e] = (hi ? vb : va) + __shfl_xor_sync(0xffffffffu, hi ? va : vb, 16);
+            }
+          }
+          double v[8];
+          {
+            const bool hi = (lane & 8) != 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[e] = double((hi ? v16[e + 8] : v16[e]) + __shfl_xor_sync(0xffffffffu, hi ? v16[e] : v16[e + 8], 8));
+          }
+#pragma unroll
+          for (int off = 4; off >= 1; off >>= 1) {
             const bool hi = (lane & off) != 0;
 #pragma unroll
             for (int e = 0; e < off; ++e) {
@@ -1414,7 +1537,61 @@ struct Sweeper {
   // Thread per row, 16 independent accumulators per pass (throughput- not latency-bound).
   __device__ double pgrad_w() {
     double acc = 0.0;
-    if constexpr (!QS && LREG > 0) {
+    if constexpr (F32S) {
+      // fp32: E (fp64, replicated) -> fp32 copy in shared memory; per row the float4 columns of Q,
+      // the row's W from the column-major scratch, grad_W(r, j0..j0+7) by fp32 FMA
+      const int k8 = (k + 7) & ~7;  // row stride of the fp32 copy: zero pad, 16-byte rows
+      for (int e = tid; e < l * k8; e += kSwThreads) {
+        const int i = e / k8, j = e % k8;
+        ef[e] = j < k ? float(Em[i * kp + j]) : 0.f;
+      }
+      __syncthreads();
+      constexpr int L4 = LREG / 4;
+      const float4* q4 = reinterpret_cast<const float4*>(a.q4);
+      for (int64_t r = tid; r < R; r += kSwThreads) {
+        float4 qv[L4];
+#pragma unroll
+        for (int i4 = 0; i4 < L4; ++i4) qv[i4] = __ldg(q4 + int64_t(i4) * a.m + r0 + r);
+        float accf = 0.f;
+        for (int j0 = 0; j0 < k; j0 += 8) {
+          float sacc[8], wv[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            sacc[t] = 0.f;
+            wv[t] = j0 + t < k ? a.wc[int64_t(j0 + t) * a.m + r0 + r] : 0.f;
+          }
+#pragma unroll
+          for (int i4 = 0; i4 < L4; ++i4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int i = 4 * i4 + c;
+              if (i < l) {
+                const float qv1 = c == 0 ? qv[i4].x : c == 1 ? qv[i4].y : c == 2 ? qv[i4].z : qv[i4].w;
+                const float4* ei = reinterpret_cast<const float4*>(ef + i * k8 + j0);
+                const float4 e0 = ei[0], e1 = ei[1];
+                sacc[0] = fmaf(qv1, e0.x, sacc[0]);
+                sacc[1] = fmaf(qv1, e0.y, sacc[1]);
+                sacc[2] = fmaf(qv1, e0.z, sacc[2]);
+                sacc[3] = fmaf(qv1, e0.w, sacc[3]);
+                sacc[4] = fmaf(qv1, e1.x, sacc[4]);
+                sacc[5] = fmaf(qv1, e1.y, sacc[5]);
+                sacc[6] = fmaf(qv1, e1.z, sacc[6]);
+                sacc[7] = fmaf(qv1, e1.w, sacc[7]);
+              }
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (j0 + t < k) {
+              const float gv = -2.f * sacc[t];
+              const float gp = wv[t] > 0.f ? gv : fminf(0.f, gv);
+              accf = fmaf(gp, gp, accf);
+            }
+          }
+        }
+        acc += double(accf);
+      }
+    } else if constexpr (!QS && LREG > 0) {
       constexpr int UNR = (sizeof(T) == 4 && LREG <= 32) ? 4 : 1;
       for (int64_t rb = tid; rb < R; rb += int64_t(kSwThreads) * UNR) {
         T qf[UNR][LREG];
@@ -1634,7 +1811,29 @@ __global__ void __launch_bounds__(kSwThreads, 1) rhals_sweeps_kernel(SweepArgs<T
   s.run();
 }
 
+// q4[i4 * m + r] = Q(r, 4 i4 .. 4 i4 + 3), zero past l (the fp32 streamed sweep path's layout)
+__global__ void relayout_q_kernel(const float* __restrict__ q, int64_t m, int l, int l4, float4* __restrict__ q4) {
+  const int64_t total = m * l4;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i4 = e / m, r = e % m;
+    const float* src = q + r * l + 4 * i4;
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = 4 * i4 + c < l ? src[c] : 0.f;
+    q4[e] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 }  // namespace
+
+int sweep_relayout_q(const float* q, int64_t m, int l, int l_pad, float* q4, cudaStream_t stream) {
+  const int l4 = l_pad / 4;
+  const int64_t total = m * l4;
+  const int blocks = int(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  if (total > 0) relayout_q_kernel<<<blocks, 256, 0, stream>>>(q, m, l, l4, reinterpret_cast<float4*>(q4));
+  RNMF_CUDA(cudaGetLastError());
+  return total > 0 ? 1 : 0;
+}
 
 template <typename T>
 SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem) {
@@ -1652,7 +1851,18 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
       p.grid = G;
       if (p.q_in_smem && p.rows_per_cta <= kSwThreads && l + 1 <= 64 && !std::getenv("RNMF_NO_QREG"))
         p.lreg = (l + 1 <= 32) ? 32 : (l + 1 <= 48) ? 48 : 64;
-      if (!p.q_in_smem && !std::getenv("RNMF_NO_QSTREAM") && (l + 1 <= 32 || (sizeof(T) == 4 && l + 1 <= 64))) {
+      if (!p.q_in_smem && sizeof(T) == 4 && !std::getenv("RNMF_NO_QSTREAM") && l <= 96) {
+        // fp32 streamed path: float4-column Q, fp32 FMA, column-major W scratch
+        const int lp = l <= 32 ? 32 : l <= 64 ? 64 : 96;
+        const SmemLayout LF = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, false, 0, lp);
+        if (LF.total <= size_t(max_smem)) {
+          p.f32s = true;
+          p.lreg = lp;
+          p.smem = LF.total;
+        }
+        return p;
+      }
+      if (!p.q_in_smem && !std::getenv("RNMF_NO_QSTREAM") && sizeof(T) == 8 && l + 1 <= 32) {
         p.lreg = (l + 1 <= 32) ? 32 : 64;
         // bulk-copy ring for the streamed slab: 16-byte row pitch, the ring must fit as well
         for (int st = kQRingMax; st >= 2 && !p.qring; --st) {
@@ -1673,8 +1883,10 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
 template <typename T>
 int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream, bool zero_sync) {
   if (plan.grid <= 0) throw CudaError("sweeps: problem does not fit the persistent kernel");
-  const SmemLayout L =
-      make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem, plan.qring);
+  const SmemLayout L = make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem, plan.qring,
+                                     plan.f32s ? plan.lreg : 0);
+  if (plan.f32s && (args.q4 == nullptr || args.wc == nullptr))
+    throw CudaError("sweeps: fp32 streamed path needs the q4 / wc buffers");
   if (zero_sync) RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, kSweepSyncBytes, stream));
   if (args.l + 1 > kColAccMax) throw CudaError("sweeps: sketch width above the column-reduction capacity");
   SweepArgs<T> a = args;
@@ -1685,9 +1897,14 @@ int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t 
   int64_t RM = plan.rows_per_cta, NCM = plan.cols_per_cta;
   void* kargs[] = {&a, const_cast<SmemLayout*>(&L), &RM, &NCM};
   const void* stream64 = nullptr;
-  if constexpr (sizeof(T) == 4) stream64 = reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 64>);
+  const void* stream96 = nullptr;
+  if constexpr (sizeof(T) == 4) {
+    stream64 = reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 64>);
+    stream96 = reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 96>);
+  }
   const void* fn = !plan.q_in_smem ? (plan.lreg == 32   ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 32>)
                                       : plan.lreg == 64 ? stream64
+                                      : plan.lreg == 96 ? stream96
                                                         : reinterpret_cast<const void*>(rhals_sweeps_kernel<T, false, 0>))
                    : plan.lreg == 32 ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true, 32>)
                    : plan.lreg == 48 ? reinterpret_cast<const void*>(rhals_sweeps_kernel<T, true, 48>)

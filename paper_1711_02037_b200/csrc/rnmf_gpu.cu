@@ -917,6 +917,20 @@ struct LoopIO {
   bool init_wt;
 };
 
+// fp32 streamed sweep path (SweepPlan::f32s): the float4-column copy of Q (once per Q, i.e. per fit
+// or stage call) and the column-major W scratch.  Returns the kernel launches issued.
+template <typename T>
+static int attach_sweep_stream(rnmf_gpu_context* ctx, const SweepPlan& plan, SweepArgs<T>& a, cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (!plan.f32s) return 0;
+    float* q4 = ctx->d<float>("sw.q4", size_t(a.m) * size_t(plan.lreg));
+    a.q4 = q4;
+    a.wc = ctx->d<float>("sw.wc", size_t(a.m) * size_t(a.k));
+    return sweep_relayout_q(a.q, a.m, a.l, plan.lreg, q4, st);
+  }
+  return 0;
+}
+
 // Row-sharded launches: zero this GPU's sync block, then an NCCL all-reduce, so that no GPU's
 // kernel can add into a peer's sync block before that peer has zeroed it for this launch.
 template <typename T>
@@ -969,6 +983,7 @@ static void run_loop(rnmf_gpu_context* ctx, Engine<T>& eng, Timer& tm, const rnm
   a.barrier = reinterpret_cast<unsigned*>(ctx->sync_block);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+  tm.launches += attach_sweep_stream<T>(ctx, plan, a, st);
   if (eng.sharded()) {
     // row-sharded: column steps and W-side sums run over every CTA of every GPU
     a.world = ctx->shard.world;
@@ -1384,6 +1399,7 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
     const int64_t plen = sweep_part_len(l, k);
     a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
     a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+    tm.launches += attach_sweep_stream<T>(ctx, plan, a, ctx->stream);
     tm.span(kInit, [&] { tm.launches += launch_sweeps_synced<T>(ctx, eng, a, plan, ctx->stream); });
     eng.export_(q_out, location, q, size_t(m) * l);
     eng.export_(b_out, location, b, size_t(l) * n);
@@ -1584,6 +1600,7 @@ static void stage_impl(rnmf_gpu_context* ctx, int location, const rnmf_problem_s
   const int64_t plen = sweep_part_len(l, k);
   a.part = ctx->d<double>("sw.part", size_t(2 * plen * plan.grid));
   a.fin = ctx->d<double>("sw.fin", size_t(2 * plen));
+  tm.launches += attach_sweep_stream<T>(ctx, plan, a, ctx->stream);
   tm.span(kSweeps, [&] { tm.launches += launch_sweeps<T>(a, plan, ctx->stream); });
   if (do_w) {
     T* wt_cast = ctx->d<T>("st.wt.cast", size_t(l) * k);

@@ -63,9 +63,12 @@ def _report(name, mode, res, ref):
     return dev
 
 
-@pytest.mark.parametrize("mode", ["exact", "tf32x3"])
+@pytest.mark.parametrize("mode", ["exact", "tf32x3", "tf32x3-streamed"])
 @pytest.mark.parametrize("name", ["C2", "C3", "C4slice"])
-def test_config_parity(gpu, name, mode):
+def test_config_parity(gpu, name, mode, monkeypatch):
+    if mode == "tf32x3-streamed":
+        # the Q slab streamed from L2 (the 1-GPU C4 path) even where it would fit on chip
+        monkeypatch.setenv("RNMF_FORCE_NOQS", "1")
     d, ref, o = _load(name)
     x = _x(name)
     x64 = x.astype(np.float64)

@@ -233,6 +233,20 @@ def test_stage_shape_errors(gpu):
         gpu.rhals_update_H(cp)
 
 
+@pytest.mark.parametrize("k,p", [(40, 20), (20, 70)])
+def test_fp32_streamed_sweeps_wide(gpu, oracle, k, p, monkeypatch):
+    """fp32 streamed-Q sweep path (float4-column Q, fp32 FMA lift / recompress, column-major W
+    scratch) at sketch widths 60 and 90 (padded widths 64 and 96), against the oracle."""
+    monkeypatch.setenv("RNMF_FORCE_NOQS", "1")
+    m, n = 3000, 700
+    x = oracle.synth_lowrank(m, n, k, 0.1, 31 + k)
+    o = _opts(gpu, rank=k, max_iter=30, tol=1e-300, oversampling=p, seed=5)
+    om, w0, h0 = workloads.injected_inputs(6, m, n, k, k + p)
+    ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    res = gpu.rhals_fit(x.astype(np.float32), o, omega=om, w0=w0, h0=h0)
+    assert_trace_close(res.trace, ref.trace, F32_TRACE_RTOL, F32_FINAL_ATOL)
+
+
 @pytest.mark.parametrize("knobs", [{"RNMF_NO_QREG": "1"}, {"RNMF_FORCE_NOQS": "1"},
                                    {"RNMF_FORCE_NOQS": "1", "RNMF_NO_QSTREAM": "1"}])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
