@@ -118,7 +118,8 @@ int tc_npad(int c);               // UMMA N for c output columns (multiple of 16
 void tc_set_chunk(int stages);    // K stages per TMEM accumulation chunk (tests / probes)
 int64_t tc_st_pitch(int64_t n);   // pitch of the S^T operand
 // S (n x c) -> S^T split into tf32 hi and fp32 lo parts (tc_npad(c) x tc_st_pitch(n) each)
-int launch_tc_prep_st(const float* s, int64_t n, int c, float* st_hi, float* st_lo, cudaStream_t stream);
+int launch_tc_prep_st(const float* s, int64_t n, int c, float* st_hi, float* st_lo, cudaStream_t stream,
+                      bool raw);
 // Y (m x c) = X (m x n, pitch ldx) * S; x3 = 3xTF32 (fp32-accurate), else 1xTF32
 int launch_tc_xw(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo, int c,
                  float* y, bool x3, int sm_count, cudaStream_t stream);
@@ -165,7 +166,7 @@ int launch_nndsvd_apply(const T* s, int64_t rows, int l, bool transpose, const d
                         const double* colscale, const double* coef, double fill, T* out, bool out_transposed,
                         cudaStream_t stream);
 
-// ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cu) -----------------------------
+// ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cuh) ----------------------------
 enum SweepFlags : int {
   kInitWt = 1,    // W~ <- Q^T W
   kInitWn = 2,    // wn <- diag(W^T W)

@@ -1,4 +1,4 @@
-// kernels_sweeps.cu — the compressed HALS loop as ONE persistent, cooperatively launched kernel.
+// kernels_sweeps.cuh — the compressed HALS loop as ONE persistent, cooperatively launched kernel.
 //
 // Restates, per sweep (UpdateOrder::Grouped):
 //   rhals_update_W   p/src/rhals.cpp:107-114 -> rhals_w_component :23-32
@@ -941,7 +941,7 @@ struct Sweeper {
       // Q(r,:)^T w, ||w||^2 in fp32 FMA (per-thread partials over a few rows), then the warp
       // reduce-scatter switches to fp64 after two levels (partials over <= 4 threads' rows in fp32)
       constexpr int L4 = LREG / 4;
-      constexpr int UNR = LREG <= 32 ? 2 : 1;
+      constexpr int UNR = LREG <= 32 ? 4 : LREG <= 64 ? 2 : 1;  // rows whose loads are in flight together
       float acc[LREG];
       float accn = 0.f;
 #pragma unroll
@@ -1480,6 +1480,61 @@ struct Sweeper {
     // CTA partial products: [T (l k) | V (k k) | E (l k) | objc | pgh]
     const int lk = l * k, kk = k * k, L = 2 * lk + kk + 2;
     double* p = part_base();
+    if constexpr (sizeof(T) == 4) {
+      // [T; V; E] = [B; H; R] H^T over this CTA's columns: rows a of the stacked operand map to
+      // partial index a k + j.  4 x 8 output tiles per thread, fp32 products summed in blocks of 32
+      // columns (the operands are fp32-rounded already) and the blocks added in fp64 -- no fp64
+      // conversion per product.
+      // (2 x 8 tiles on the register-resident Q path, whose Q rows occupy 128 registers)
+      constexpr int TI = (QS && LREG >= 64) ? 2 : 4;
+      const int AR = 2 * l + k;
+      const int ntJ = (k + 7) / 8, ntiles = ((AR + TI - 1) / TI) * ntJ;
+      for (int tile = tid; tile < ntiles; tile += kSwThreads) {
+        const int a0 = (tile / ntJ) * TI, j0 = (tile % ntJ) * 8;
+        const T* ap[TI];
+        const T* hp[8];
+#pragma unroll
+        for (int u = 0; u < TI; ++u) {
+          const int ar = min(a0 + u, AR - 1);
+          ap[u] = ar < l ? Bc + ar * ncp : ar < l + k ? Hc + (ar - l) * ncp : Rc + (ar - l - k) * ncp;
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) hp[v] = Hc + min(j0 + v, k - 1) * ncp;
+        double accd[TI][8];
+#pragma unroll
+        for (int u = 0; u < TI; ++u)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) accd[u][v] = 0.0;
+        for (int64_t cb = 0; cb < NC; cb += 32) {
+          const int64_t ce = min(NC, cb + 32);
+          float accf[TI][8];
+#pragma unroll
+          for (int u = 0; u < TI; ++u)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) accf[u][v] = 0.f;
+          for (int64_t c = cb; c < ce; ++c) {
+            float av[TI], hv[8];
+#pragma unroll
+            for (int u = 0; u < TI; ++u) av[u] = float(ap[u][c]);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) hv[v] = float(hp[v][c]);
+#pragma unroll
+            for (int u = 0; u < TI; ++u)
+#pragma unroll
+              for (int v = 0; v < 8; ++v) accf[u][v] = fmaf(av[u], hv[v], accf[u][v]);
+          }
+#pragma unroll
+          for (int u = 0; u < TI; ++u)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) accd[u][v] += double(accf[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < TI; ++u)
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            if (a0 + u < AR && j0 + v < k) p[int64_t(g) * L + (a0 + u) * k + j0 + v] = accd[u][v];
+      }
+    } else
     for (int e = tid; e < 2 * lk + kk; e += kSwThreads) {
       const T *xa, *xb;
       if (e < lk) {
@@ -1811,6 +1866,10 @@ __global__ void __launch_bounds__(kSwThreads, 1) rhals_sweeps_kernel(SweepArgs<T
   s.run();
 }
 
+}  // namespace
+
+#ifdef RNMF_SWEEPS_COMMON
+namespace {
 // q4[i4 * m + r] = Q(r, 4 i4 .. 4 i4 + 3), zero past l (the fp32 streamed sweep path's layout)
 __global__ void relayout_q_kernel(const float* __restrict__ q, int64_t m, int l, int l4, float4* __restrict__ q4) {
   const int64_t total = m * l4;
@@ -1834,6 +1893,7 @@ int sweep_relayout_q(const float* q, int64_t m, int l, int l_pad, float* q4, cud
   RNMF_CUDA(cudaGetLastError());
   return total > 0 ? 1 : 0;
 }
+#endif
 
 template <typename T>
 SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem) {
@@ -1918,11 +1978,12 @@ int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t 
   return 1;
 }
 
-template SweepPlan plan_sweeps<float>(int64_t, int64_t, int, int, int, int);
-template SweepPlan plan_sweeps<double>(int64_t, int64_t, int, int, int, int);
-template int launch_sweeps<float>(const SweepArgs<float>&, const SweepPlan&, cudaStream_t, bool);
-template int launch_sweeps<double>(const SweepArgs<double>&, const SweepPlan&, cudaStream_t, bool);
-
+#ifdef RNMF_SWEEPS_T
+template SweepPlan plan_sweeps<RNMF_SWEEPS_T>(int64_t, int64_t, int, int, int, int);
+template int launch_sweeps<RNMF_SWEEPS_T>(const SweepArgs<RNMF_SWEEPS_T>&, const SweepPlan&, cudaStream_t, bool);
+#endif
+#ifdef RNMF_SWEEPS_COMMON
 bool sweep_prof_compiled() { return kSweepProf; }
+#endif
 
 }  // namespace rnmf_gpu

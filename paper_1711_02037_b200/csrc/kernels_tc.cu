@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
     // ---------------- TMA producer
     if (tc::elect_one()) {
       uint32_t it = 0;
-      const uint32_t bytes = uint32_t(C::kStageBytes);
+      // 3xTF32: only the raw S^T slab comes from L2; the split warps write its lo slab on chip
+      const uint32_t bytes = uint32_t(kXTileBytes + C::kSBytes);
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
@@ -252,7 +253,6 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
           tc::mbar_arrive_expect_tx(&sm.full[s], bytes);
           tc::tma_load_2d(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM));
           tc::tma_load_2d(sm.shi(s), &tmShi, &sm.full[s], kc * kBK, 0);
-          if (X3) tc::tma_load_2d(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0);
         }
       }
     }
@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
           tc::mbar_wait(&sm.full[s], (it / S) & 1);
           tc::mbar_wait(&sm.loempty[j], ((it / kLoSlots) & 1) ^ 1);
           split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(sm.x(s)), reinterpret_cast<float4*>(sm.lo(j)), st);
+          split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(sm.shi(s)), reinterpret_cast<float4*>(sm.slo(s)), st);
           tc::fence_proxy_async_smem();
           tc::mbar_arrive(&sm.lofull[j]);
         }
@@ -391,11 +392,11 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
         for (int64_t r = r0; r < r1; r += kBK, ++it) {
           const int s = int(it % S);
           tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(C::kStageBytes));
+          // 3xTF32: the raw S^T slab only; its lo slab is written on chip by the split warps
+          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes + C::kSBytes));
 #pragma unroll
           for (int b = 0; b < 4; ++b) tc::tma_load_2d(sm.x(s) + b * 4096, &tmX, &sm.full[s], int(ct * 128 + b * 32), int(r));
           tc::tma_load_2d(sm.shi(s), &tmSt, &sm.full[s], int(r), 0);
-          if (X3) tc::tma_load_2d(sm.slo(s), &tmStLo, &sm.full[s], int(r), 0);
         }
       }
     }
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
           tc::mbar_wait(&sm.full[s], (it / S) & 1);
           tc::mbar_wait(&sm.loempty[j], ((it / kLoSlots) & 1) ^ 1);
           split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(sm.x(s)), reinterpret_cast<float4*>(sm.lo(j)), st);
+          split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(sm.shi(s)), reinterpret_cast<float4*>(sm.slo(s)), st);
           tc::fence_proxy_async_smem();
           tc::mbar_arrive(&sm.lofull[j]);
         }
@@ -498,18 +500,24 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
   }
 }
 
-// S (n x c, row-major, ld c) -> S^T hi / lo (npad x ldst, zero rows for j >= c and cols >= n):
-// hi = rna_tf32(s) (exact tf32, the operand of 1xTF32 too), lo = rna_tf32(s - hi)
+// S (n x c, row-major, ld c) -> S^T hi / lo (npad x ldst, zero rows for j >= c and cols >= n).
+// 3xTF32 (raw): hi = s itself (kind::tf32 truncates it) and lo = rna_tf32(s - trunc_tf32(s)), the
+// split the kernels also apply on chip to X and to the S slabs; 1xTF32: hi = rna_tf32(s).
 __global__ void prep_st_kernel(const float* __restrict__ s, int64_t n, int c, int npad, int64_t ldst,
-                               float* __restrict__ st_hi, float* __restrict__ st_lo) {
+                               float* __restrict__ st_hi, float* __restrict__ st_lo, bool raw) {
   const int64_t total = int64_t(npad) * ldst;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     const int j = int(e / ldst);
     const int64_t kk = e % ldst;
     const float v = (j < c && kk < n) ? s[kk * c + j] : 0.f;
-    const float h = tc::tf32_hi(v);
-    st_hi[e] = h;
-    st_lo[e] = tc::tf32_hi(v - h);
+    if (raw) {
+      st_hi[e] = v;
+      st_lo[e] = tf32_lo(v);
+    } else {
+      const float h = tc::tf32_hi(v);
+      st_hi[e] = h;
+      st_lo[e] = tc::tf32_hi(v - h);
+    }
   }
 }
 
@@ -658,11 +666,11 @@ void tc_set_chunk(int stages) { g_tc_chunk = stages; }
 
 int64_t tc_st_pitch(int64_t n) { return ceil_div(n, 32) * 32; }
 
-int launch_tc_prep_st(const float* s, int64_t n, int c, float* st_hi, float* st_lo, cudaStream_t stream) {
+int launch_tc_prep_st(const float* s, int64_t n, int c, float* st_hi, float* st_lo, cudaStream_t stream, bool raw) {
   const int npad = tc_npad(c);
   const int64_t ld = tc_st_pitch(n);
   const int blocks = int(std::min<int64_t>(ceil_div(int64_t(npad) * ld, 256), 148 * 8));
-  prep_st_kernel<<<blocks, 256, 0, stream>>>(s, n, c, npad, ld, st_hi, st_lo);
+  prep_st_kernel<<<blocks, 256, 0, stream>>>(s, n, c, npad, ld, st_hi, st_lo, raw);
   RNMF_CUDA_LAUNCH();
   return 1;
 }
@@ -904,9 +912,8 @@ __global__ void tc_resid_prep_kernel(const float* __restrict__ w, int64_t m, con
       hi = ht_hi + f;
       lo = ht_lo + f;
     }
-    const float vh = tc::tf32_hi(v);
-    *hi = vh;
-    *lo = tc::tf32_hi(v - vh);
+    *hi = v;  // raw hi (truncated by kind::tf32), lo = what the truncation drops
+    *lo = tf32_lo(v);
   }
 }
 
@@ -917,9 +924,8 @@ __global__ void tc_prep_rows_kernel(const float* __restrict__ src, int c, int64_
     const int j = int(e / ldst);
     const int64_t kk = e % ldst;
     const float v = (j < c && kk < n) ? src[int64_t(j) * n + kk] : 0.f;
-    const float h = tc::tf32_hi(v);
-    st_hi[e] = h;
-    st_lo[e] = tc::tf32_hi(v - h);
+    st_hi[e] = v;  // raw hi (truncated by kind::tf32), lo = what the truncation drops
+    st_lo[e] = tf32_lo(v);
   }
 }
 
@@ -1002,9 +1008,8 @@ __global__ void tc_metrics_prep_kernel(const float* __restrict__ w, const float*
       hi = sw_hi + f;
       lo = sw_lo + f;
     }
-    const float vh = tc::tf32_hi(v);
-    *hi = vh;
-    *lo = tc::tf32_hi(v - vh);
+    *hi = v;  // raw hi (truncated by kind::tf32), lo = what the truncation drops
+    *lo = tf32_lo(v);
   }
 }
 
@@ -1210,12 +1215,11 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
+          // raw H and H^T slabs only; the split warps write their lo slabs on chip
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(kXTileBytes + C::kSBytes + 4096));
           tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
           tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
-          tc::tma_load_2d(shi(s) + C::kSBytes, &tmSlo, &full[s], kc * kBK, 0);
           tc::tma_load_2d(htp(s), &tmHhi, &full[s], 0, kc * kBK);
-          tc::tma_load_2d(htp(s) + 4096, &tmHlo, &full[s], 0, kc * kBK);
         }
       }
     }
@@ -1275,6 +1279,8 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
         tc::mbar_wait(&full[s], (it / S) & 1);
         tc::mbar_wait(&loempty[j], ((it / kLoSlots) & 1) ^ 1);
         split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(xst(s)), reinterpret_cast<float4*>(lo(j)), st);
+        split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(shi(s)), reinterpret_cast<float4*>(shi(s) + C::kSBytes), st);
+        split_lo_tile<256>(reinterpret_cast<const float4*>(htp(s)), reinterpret_cast<float4*>(htp(s) + 4096), st);
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&lofull[j]);
       }
@@ -1374,6 +1380,285 @@ void tc_xht_resid_launch(const float* x, int64_t m, int64_t n, int64_t ldx, cons
   RNMF_CUDA_LAUNCH();
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused metrics pass for 32 < k <= 64: as tc_xht_resid_kernel (X H^T by 3xTF32 into TMEM chunks
+// drained to fp32 registers, and sum (X - W H)^2 per stage), but the W tile (hi, lo; K = 8 ks
+// columns each) is the A operand from TENSOR MEMORY: the epilogue threads store their row of W_hi /
+// W_lo with tcgen05.st at the start of each row tile, which keeps shared memory for a deep X ring.
+// TMEM columns: [0, 4 NPAD) X H^T chunk buffers | kRb x 64 W H ring | W_hi (64) | W_lo (64).
+// Shared: ring stage = [X 16 KB][H slab hi | lo (NPAD rows each)][H^T slab, two 32-wide K atoms of
+// (32 hi rows | 32 lo rows)]; kLoW lo-X slots.
+template <int NPAD>
+struct FwCfg {
+  static constexpr int kSBytes = NPAD * kBK * 4;
+  static constexpr int kHtBytes = 2 * (2 * 32 * 128);  // 2 K atoms x (hi | lo)
+  static constexpr int kStageBytes = kXTileBytes + 2 * kSBytes + kHtBytes;
+  static constexpr int kLoW = 2;
+  static constexpr int kLoBytes = kLoW * kXTileBytes;
+  static constexpr int kStages = std::min(6, (226 * 1024 - kLoBytes - 2048) / kStageBytes);
+  static constexpr int kAccCols = 2 * NPAD;
+  static constexpr int kRsBase = 2 * kAccCols;
+  static constexpr int kRb = (512 - kRsBase - 128) / 64;  // W H ring depth
+  static constexpr int kWBase = kRsBase + kRb * 64;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kLoBytes + 1024 + 512;
+  static_assert(kStages >= 3 && kRb >= 2 && kWBase + 128 <= 512, "layout");
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
+    const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmShi,
+    const __grid_constant__ CUtensorMap tmSlo, const __grid_constant__ CUtensorMap tmHhi,
+    const __grid_constant__ CUtensorMap tmHlo, const float* __restrict__ w_hi, const float* __restrict__ w_lo,
+    int ks, FzParams p) {
+  using C = FwCfg<NPAD>;
+  constexpr int S = C::kStages;
+  constexpr int LO = C::kLoW;
+  constexpr int RB = C::kRb;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  auto xst = [&](int s) { return base + size_t(s) * C::kStageBytes; };
+  auto shi = [&](int s) { return xst(s) + kXTileBytes; };
+  auto htp = [&](int s) { return shi(s) + 2 * C::kSBytes; };
+  auto lo = [&](int j) { return base + size_t(S) * C::kStageBytes + size_t(j) * kXTileBytes; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + size_t(S) * C::kStageBytes + C::kLoBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + S;
+  uint64_t* lofull = empty + S;
+  uint64_t* loempty = lofull + LO;
+  uint64_t* tfull = loempty + LO;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + RB;
+  uint64_t* wfull = rempty + RB;
+  uint64_t* wempty = wfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+  double* red = reinterpret_cast<double*>(wempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = ceil_div(p.m, kBM);
+  const int nk = int(ceil_div(p.n, kBK));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1 + 4);
+    }
+    for (int j = 0; j < LO; ++j) {
+      tc::mbar_init(&lofull[j], kSplitThreads);
+      tc::mbar_init(&loempty[j], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 128);
+    }
+    for (int b = 0; b < RB; ++b) {
+      tc::mbar_init(&rfull[b], 1);
+      tc::mbar_init(&rempty[b], 128);
+    }
+    tc::mbar_init(wfull, 128);
+    tc::mbar_init(wempty, 1);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmShi);
+    tc::tma_prefetch(&tmSlo);
+    tc::tma_prefetch(&tmHhi);
+    tc::tma_prefetch(&tmHlo);
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = int(it % S);
+          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          // raw H and H^T slabs only; the split warps write their lo slabs on chip
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(kXTileBytes + C::kSBytes + 2 * 4096));
+          tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
+          tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
+#pragma unroll
+          for (int a = 0; a < 2; ++a) tc::tma_load_2d(htp(s) + a * 8192, &tmHhi, &full[s], a * 32, kc * kBK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc32 = tc::make_idesc_tf32(32, false, false);
+    constexpr uint32_t idesc64 = tc::make_idesc_tf32(64, false, false);
+    auto adesc = [](uint32_t b, int k) { return tc::make_sdesc(b + k * 32, 16, 1024); };
+    uint32_t it = 0, ci = 0, ti = 0;
+    uint32_t d = tmem_base;
+    const uint32_t wa_hi = tmem_base + uint32_t(C::kWBase), wa_lo = wa_hi + 64u;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+      tc::mbar_wait(wfull, ti & 1);  // this tile's W rows are in TMEM
+      tc::tc_fence_after();
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int kin = kc % p.chunk;
+        const bool cend = (kin == p.chunk - 1) || (kc == nk - 1);
+        const int acc = int(ci & 1);
+        if (kin == 0) {
+          tc::mbar_wait(&tempty[acc], ((ci >> 1) & 1) ^ 1);
+          d = tmem_base + uint32_t(acc * C::kAccCols);
+        }
+        const int s = int(it % S), j = int(it % LO), b = int(it % RB);
+        tc::mbar_wait(&rempty[b], ((it / RB) & 1) ^ 1);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&lofull[j], (it / LO) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          issue_stage<NPAD, true, false>(d, tc::smem_u32(xst(s)), tc::smem_u32(lo(j)), tc::smem_u32(shi(s)), kin == 0,
+                                         adesc);
+          const uint32_t dr = tmem_base + uint32_t(C::kRsBase + b * 64);
+          const uint32_t ha = tc::smem_u32(htp(s));
+          for (int kk = 0; kk < ks; ++kk) {
+            const uint64_t hb = tc::make_sdesc(ha + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
+            tc::umma_tf32_ts(dr, wa_hi + uint32_t(kk * 8), hb, idesc64, kk != 0);  // [W_hi H_hi | W_hi H_lo]
+            tc::umma_tf32_ts(dr + 32, wa_lo + uint32_t(kk * 8), hb, idesc32, 1u);  // += W_lo H_hi
+          }
+          tc::umma_commit(&empty[s]);
+          tc::umma_commit(&loempty[j]);
+          tc::umma_commit(&rfull[b]);
+          if (cend) tc::umma_commit(&tfull[acc]);
+          if (kc == nk - 1) tc::umma_commit(wempty);
+        }
+        if (cend) ++ci;
+        __syncwarp();
+      }
+    }
+  } else if (warp < 4 || warp >= 8) {
+    const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = int(it % S), j = int(it % LO);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&loempty[j], ((it / LO) & 1) ^ 1);
+        split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(xst(s)), reinterpret_cast<float4*>(lo(j)), st);
+        split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(shi(s)), reinterpret_cast<float4*>(shi(s) + C::kSBytes), st);
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          split_lo_tile<256>(reinterpret_cast<const float4*>(htp(s) + a * 8192), reinterpret_cast<float4*>(htp(s) + a * 8192 + 4096), st);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&lofull[j]);
+      }
+    }
+  } else {
+    const int sub = warp & 3;
+    const int r = sub * 32 + lane;
+    const uint32_t lane_off = uint32_t(sub * 32) << 16;
+    double racc = 0.0;
+    uint32_t it = 0, ci = 0, ti = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
+      const int64_t row = t * kBM + r;
+      {
+        // W row (hi, lo; 64 columns each, zero past k and past m) into TMEM once the previous
+        // tile's UMMAs are done with it
+        tc::mbar_wait(wempty, (ti & 1) ^ 1);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int part = 0; part < 4; ++part) {
+          const float* src = (part < 2 ? w_hi : w_lo) + row * 64 + (part & 1) * 32;
+          uint32_t v[32];
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < p.m) f = __ldg(reinterpret_cast<const float4*>(src) + q4);
+            v[4 * q4] = __float_as_uint(f.x), v[4 * q4 + 1] = __float_as_uint(f.y);
+            v[4 * q4 + 2] = __float_as_uint(f.z), v[4 * q4 + 3] = __float_as_uint(f.w);
+          }
+          tc::tmem_st_32x32b_x32(tmem_base + lane_off + uint32_t(C::kWBase + part * 32), v);
+        }
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(wfull);
+      }
+      float a[NPAD];
+#pragma unroll
+      for (int q = 0; q < NPAD; ++q) a[q] = 0.f;
+      for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int s = int(it % S), b = int(it % RB);
+        tc::mbar_wait(&full[s], (it / S) & 1);
+        tc::mbar_wait(&rfull[b], (it / RB) & 1);
+        tc::tc_fence_after();
+        uint32_t d0[32], d1[32];
+        const uint32_t taddr = tmem_base + lane_off + uint32_t(C::kRsBase + b * 64);
+        tc::tmem_ld_32x32b_x32(taddr, d0);
+        tc::tmem_ld_32x32b_x32(taddr + 32, d1);
+        const uint32_t xrow = tc::smem_u32(xst(s)) + uint32_t(r) * 128u;
+        float xv[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t v0, v1, v2, v3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)));
+          xv[4 * c] = __uint_as_float(v0), xv[4 * c + 1] = __uint_as_float(v1);
+          xv[4 * c + 2] = __uint_as_float(v2), xv[4 * c + 3] = __uint_as_float(v3);
+        }
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&rempty[b]);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        float ss = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float e = xv[c] - (__uint_as_float(d0[c]) + __uint_as_float(d1[c]));
+          ss = fmaf(e, e, ss);
+        }
+        racc += double(ss);
+        const bool cend = (kc % p.chunk == p.chunk - 1) || (kc == nk - 1);
+        if (cend) {
+          const int acc = int(ci & 1);
+          tc::mbar_wait(&tfull[acc], (ci >> 1) & 1);
+          tc::tc_fence_after();
+          drain_acc<NPAD, true>(tmem_base + lane_off + uint32_t(acc * C::kAccCols), a);
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[acc]);
+          ++ci;
+        }
+      }
+      if (row < p.m) {
+#pragma unroll
+        for (int q = 0; q < NPAD; ++q)
+          if (q < p.c) p.y[row * p.c + q] = a[q];
+      }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
+    if (lane == 0) red[sub] = racc;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) p.part_obj[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
+}
+
+template <int NPAD>
+void tc_xht_resid_w_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
+                           const float* w_hi, const float* w_lo, const float* ht_hi, const float* ht_lo, int k,
+                           float* xht, double* part_obj, int grid, cudaStream_t stream) {
+  using C = FwCfg<NPAD>;
+  const int64_t ldst = tc_st_pitch(n);
+  const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBM);
+  const CUtensorMap mh = make_map_2d(st_hi, NPAD, n, ldst, NPAD);
+  const CUtensorMap ml = make_map_2d(st_lo, NPAD, n, ldst, NPAD);
+  const CUtensorMap mhh = make_map_2d(ht_hi, ldst, 64, 64, 32);
+  const CUtensorMap mhl = make_map_2d(ht_lo, ldst, 64, 64, 32);
+  FzParams p{m, n, k, xht, tc_chunk_stages(), part_obj};
+  auto f = tc_xht_resid_w_kernel<NPAD>;
+  RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
+  f<<<grid, kTcThreadsX3, C::kSmem, stream>>>(mx, mh, ml, mhh, mhl, w_hi, w_lo, int(ceil_div(k, 8)), p);
+  RNMF_CUDA_LAUNCH();
+}
+
 }  // namespace
 
 int launch_tc_xht_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
@@ -1381,9 +1666,14 @@ int launch_tc_xht_resid(const float* x, int64_t m, int64_t n, int64_t ldx, const
                         double* part_obj, int* nblocks, int sm_count, cudaStream_t stream) {
   if ((ldx * sizeof(float)) % 16 != 0 || (reinterpret_cast<uintptr_t>(x) % 16) != 0)
     throw CudaError("tc_xht_resid: X needs a 16-byte aligned base and row pitch");
-  if (k > 32 || tc_resid_kw(k) != 32) throw CudaError("tc_xht_resid: k above 32");
+  if (k > 64) throw CudaError("tc_xht_resid: k above 64");
   const int grid = tc_resid_blocks(m, sm_count);
-  if (tc_npad(k) == 16)
+  if (k > 32) {  // W from tensor memory (w_hi / w_lo: m x 64, ht_hi / ht_lo: ldst x 64)
+    if (tc_npad(k) == 48)
+      tc_xht_resid_w_launch<48>(x, m, n, ldx, st_hi, st_lo, w_hi, w_lo, ht_hi, ht_lo, k, xht, part_obj, grid, stream);
+    else
+      tc_xht_resid_w_launch<64>(x, m, n, ldx, st_hi, st_lo, w_hi, w_lo, ht_hi, ht_lo, k, xht, part_obj, grid, stream);
+  } else if (tc_npad(k) == 16)
     tc_xht_resid_launch<16>(x, m, n, ldx, st_hi, st_lo, w_hi, w_lo, ht_hi, ht_lo, k, xht, part_obj, grid, stream);
   else
     tc_xht_resid_launch<32>(x, m, n, ldx, st_hi, st_lo, w_hi, w_lo, ht_hi, ht_lo, k, xht, part_obj, grid, stream);

@@ -524,7 +524,7 @@ class Engine {
       tm_.span(kXw, [&] {
         if constexpr (std::is_same<T, float>::value) {
           if (tc) {
-            tm_.launches += launch_tc_prep_st(s, n, l, st_hi, st_lo, st_);
+            tm_.launches += launch_tc_prep_st(s, n, l, st_hi, st_lo, st_, x3);
             tm_.span(kXwK, [&] { tm_.launches += launch_tc_xw(x, m, n, ldx, st_hi, st_lo, l, out, x3, ctx_->sm_count, st_); });
             return;
           }
@@ -547,7 +547,7 @@ class Engine {
       tm_.span(kXtw, [&] {
         if constexpr (std::is_same<T, float>::value) {
           if (tc) {
-            tm_.launches += launch_tc_prep_st(s, m, l, st_hi, st_lo, st_);
+            tm_.launches += launch_tc_prep_st(s, m, l, st_hi, st_lo, st_, x3);
             tm_.span(kXtwK, [&] {
               tm_.launches += launch_tc_xtw(x, m, n, ldx, st_hi, st_lo, l, part, splits, x3, ctx_->sm_count, st_);
             });
@@ -841,7 +841,7 @@ class Engine {
     double* ppgw = ctx_->d<double>("tcm.ppgw", size_t(tc_pgw_blocks(m)));
     double* ppgh = ctx_->d<double>("tcm.ppgh", size_t(grad_h_blocks(n, k)));
     double* tmp = ctx_->d<double>("met.tmp", 4);
-    const bool fused = k <= 32 && !std::getenv("RNMF_NO_FUSED_RESID");
+    const bool fused = k <= 64 && !std::getenv("RNMF_NO_FUSED_RESID");
     tm_.span(kMetrics, [&] {
       if (hht_in)
         hht = const_cast<double*>(hht_in);

@@ -78,11 +78,13 @@ def test_tf32x3_rqb_projector(gpu, oracle):
 def test_tf32x3_edge_shapes(gpu, oracle, m, n, k):
     """Tiny and ragged shapes through the tensor-core sketch and metrics kernels (partial 128-row
     tiles, fewer columns than one 32-wide stage, l clamped to min(m, n))."""
-    x = oracle.synth_lowrank(m, n, min(k, m, n), 0.1, 40 + m + n)
     o = gpu.SolverOptions(rank=k, max_iter=8, tol=1e-300, oversampling=4, power_iterations=1, seed=2)
     if k > min(m, n):
         o.rank = min(m, n)
     l = min(o.rank + 4, m, n)
+    # X of rank >= l: with rank(X) < l the trailing sketch directions are rounding noise (the C1
+    # situation, checked two-stage in test_gpu_parity) and the trace is not comparable pointwise
+    x = oracle.synth_lowrank(m, n, l, 0.1, 40 + m + n)
     om, w0, h0 = workloads.injected_inputs(5, m, n, o.rank, l)
     ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
     o.math_mode = gpu.MathMode.TF32x3

@@ -129,7 +129,7 @@ int main(int argc, char** argv) {
     };
     float ms = timeit([&] { launch_xw_tma<float>(dx, m, n, ldx, ds, c, dy, dspad, sms, 0); });
     report("ffma_tma", ms);
-    launch_tc_prep_st(ds, n, c, dh, dl, 0);
+    launch_tc_prep_st(ds, n, c, dh, dl, 0, true);
     for (int x3 = 1; x3 >= 0; --x3)
       for (int ch : {16, 8, 4}) {
         if (!x3 && ch != 2) continue;
@@ -158,7 +158,7 @@ int main(int argc, char** argv) {
     const int sp = xtw_tma_splits(m, n, sms);
     float ms = timeit([&] { launch_xtw_tma<float>(dx, m, n, ldx, dq, c, dpart, sp, dout, false, dspad, sms, 0); });
     report("ffma_tma", ms);
-    launch_tc_prep_st(dq, m, c, dh, dl, 0);
+    launch_tc_prep_st(dq, m, c, dh, dl, 0, true);
     const int tsp = tc_xtw_splits(m, n, sms);
     for (int x3 = 1; x3 >= 0; --x3)
       for (int ch : {16, 8, 4}) {

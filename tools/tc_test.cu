@@ -45,7 +45,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dy, size_t(m) * c * 4));
   CK(cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ds, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
-  launch_tc_prep_st(ds, n, c, dh, dl, 0);
+  launch_tc_prep_st(ds, n, c, dh, dl, 0, true);
   // reference on a row sample (fp64)
   std::vector<int64_t> rows;
   for (int64_t i = 0; i < m; i += std::max<int64_t>(1, m / 200)) rows.push_back(i);
@@ -108,7 +108,7 @@ int xtw_main(int64_t m, int64_t n, int c, int reps) {
   CK(cudaMalloc(&dp, size_t(splits) * n * c * 4));
   CK(cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ds, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
-  launch_tc_prep_st(ds, m, c, dh, dl, 0);
+  launch_tc_prep_st(ds, m, c, dh, dl, 0, true);
   for (int x3 = 0; x3 < 2; ++x3) {
   launch_tc_xtw(dx, m, n, ldx, dh, dl, c, dp, splits, x3, prop.multiProcessorCount, 0);
   CK(cudaDeviceSynchronize());
