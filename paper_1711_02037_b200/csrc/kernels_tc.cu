@@ -78,7 +78,7 @@ __device__ __forceinline__ void split_lo_tile(const float4* __restrict__ x4, flo
     if (q < N16)
       asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3])
-                   : "r"(xs + 16u * uint32_t(q)));
+                   : "r"(xs + 16u * uint32_t(q)) : "memory");
   }
 #pragma unroll
   for (int i = 0; i < kIt; ++i) {
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) tc_resid_kernel(const __grid_co
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1 + 4);  // UMMA commit (H slab read) + one arrival per epilogue warp (X read)
+      tc::mbar_init(&empty[s], 1 + 128);  // UMMA commit (H slab read) + every epilogue thread (X row read)
     }
     for (int b = 0; b < kRsTmemBufs; ++b) {
       tc::mbar_init(&tfull[b], 1);
@@ -860,15 +860,14 @@ __global__ void __launch_bounds__(kRsThreads, 1) tc_resid_kernel(const __grid_co
           uint32_t v0, v1, v2, v3;
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)));
+                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)) : "memory");
           xv[4 * c] = __uint_as_float(v0), xv[4 * c + 1] = __uint_as_float(v1);
           xv[4 * c + 2] = __uint_as_float(v2), xv[4 * c + 3] = __uint_as_float(v3);
         }
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         tc::mbar_arrive(&tempty[b]);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        tc::mbar_arrive(&empty[s]);  // every epilogue thread: its X row loads are done
         float ss = 0.f;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
@@ -1173,7 +1172,7 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1 + 4);
+      tc::mbar_init(&empty[s], 1 + 128);
     }
     for (int j = 0; j < kLoSlots; ++j) {
       tc::mbar_init(&lofull[j], kSplitThreads);
@@ -1313,15 +1312,14 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
           uint32_t v0, v1, v2, v3;
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)));
+                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)) : "memory");
           xv[4 * c] = __uint_as_float(v0), xv[4 * c + 1] = __uint_as_float(v1);
           xv[4 * c + 2] = __uint_as_float(v2), xv[4 * c + 3] = __uint_as_float(v3);
         }
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         tc::mbar_arrive(&rempty[b]);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        tc::mbar_arrive(&empty[s]);  // every epilogue thread: its X row loads are done
         float ss = 0.f;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
@@ -1441,7 +1439,7 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1 + 4);
+      tc::mbar_init(&empty[s], 1 + 128);
     }
     for (int j = 0; j < LO; ++j) {
       tc::mbar_init(&lofull[j], kSplitThreads);
@@ -1595,15 +1593,14 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
           uint32_t v0, v1, v2, v3;
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)));
+                       : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)) : "memory");
           xv[4 * c] = __uint_as_float(v0), xv[4 * c + 1] = __uint_as_float(v1);
           xv[4 * c + 2] = __uint_as_float(v2), xv[4 * c + 3] = __uint_as_float(v3);
         }
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         tc::mbar_arrive(&rempty[b]);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[s]);
+        tc::mbar_arrive(&empty[s]);  // every epilogue thread: its X row loads are done
         float ss = 0.f;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
