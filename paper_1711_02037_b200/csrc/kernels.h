@@ -179,6 +179,7 @@ enum SweepFlags : int {
   kReseed = 256,      // reseed_dead: liveness stamps per sweep, stop at a dead component (host reseeds)
   kEvalPrev = 512,    // evaluate + record sweep t_begin - 1 first (after a host-side reseed)
   kXFlat = 1024,      // row-sharded column step: every CTA exchanges with every GPU (testing knob)
+  kHWarpCols = 2048,  // H phase on the warp-per-column path even where lane-per-column fits (testing knob)
 };
 // Sync block of the sweep kernel (zeroed before every launch): the legacy grid-barrier counter at
 // byte 0 (cross-GPU counter at byte 64), a 3-slot ring of 64-bit fixed-point accumulators for the

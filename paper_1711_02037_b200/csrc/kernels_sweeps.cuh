@@ -1310,6 +1310,99 @@ struct Sweeper {
     __syncthreads();
   }
 
+  // H phase, one owned column per thread (clamped_row_update, p/src/hals.cpp:75-81, applied to the
+  // column's k entries in order, p/src/rhals.cpp:52-55).  g_j = (S h)_j - r_j with r = B^T W~ is
+  // kept in fp64 registers, so row update j is h_j <- [h_j - (g_j + alpha h_j + beta) / d_j]_+
+  // followed by g += S(j, :) (h_j_new - h_j): a register chain without shuffles, 32 columns per
+  // warp in flight.  Afterwards g is grad_H / 2 at the new h (grad_valid), the residual column
+  // B(:,c) - W~ h goes to Rc (objc; W~^T residc for !grad_valid), and H is stored in place.
+  template <int KH>
+  __device__ void h_cols_lane(bool update, bool grad_valid, double& objc_l, double& pgh_l,
+                              unsigned long long& hmask) {
+    const double alpha = a.alpha_h, beta = a.beta_h;
+    for (int64_t c = tid; c < NC; c += kSwThreads) {
+      double g[KH];
+#pragma unroll
+      for (int j = 0; j < KH; ++j) g[j] = 0.0;
+      // -r_j = -sum_i B(i,c) W~(i,j)
+      for (int i = 0; i < l; ++i) {
+        const double b = double(Bc[i * ncp + c]);
+        const double* wi = Wt + i * kp;
+#pragma unroll
+        for (int j = 0; j < KH; ++j)
+          if (j < k) g[j] = fma(-b, wi[j], g[j]);
+      }
+      // + (S h)_j
+      for (int i = 0; i < k; ++i) {
+        const double hi = double(Hc[i * ncp + c]);
+        const double* si = Sm + i * k;
+#pragma unroll
+        for (int j = 0; j < KH; ++j)
+          if (j < k) g[j] = fma(si[j], hi, g[j]);
+      }
+      if (update) {
+        for (int j = 0; j < k; ++j) {
+          double gj = g[0];  // g[j] without a dynamically indexed register array
+#pragma unroll
+          for (int i = 1; i < KH; ++i) gj = i == j ? g[i] : gj;
+          const double hj = double(Hc[j * ncp + c]);
+          double num = -(gj + alpha * hj);
+          if (beta != 0.0) num -= beta;
+          const double hn = fmax(0.0, hj + num * invd[j]);
+          const double d = hn - hj;
+          const T hv = T(hn);
+          Hc[j * ncp + c] = hv;
+          if (hv > T(0)) hmask |= 1ull << j;
+          const double* sj = Sm + j * k;
+#pragma unroll
+          for (int i = 0; i < KH; ++i)
+            if (i < k) g[i] = fma(sj[i], d, g[i]);
+        }
+      }
+      if (grad_valid) {
+        // grad_H = 2 (S h - r) (p/src/rhals.cpp:154), projected (p/src/hals.cpp:55-65)
+#pragma unroll
+        for (int j = 0; j < KH; ++j)
+          if (j < k) {
+            const double gv = 2.0 * g[j];
+            const double gp = Hc[j * ncp + c] > T(0) ? gv : fmin(0.0, gv);
+            pgh_l += gp * gp;
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < KH; ++j) g[j] = 0.0;  // reused for W~^T residc
+      // residc(:,c) = B(:,c) - W~ h; objc
+      for (int i = 0; i < l; ++i) {
+        const double* wi = Wt + i * kp;
+        double r0 = double(Bc[i * ncp + c]), r1 = 0.0;
+        int j = 0;
+        for (; j + 1 < k; j += 2) {
+          r0 = fma(-wi[j], double(Hc[j * ncp + c]), r0);
+          r1 = fma(-wi[j + 1], double(Hc[(j + 1) * ncp + c]), r1);
+        }
+        if (j < k) r0 = fma(-wi[j], double(Hc[j * ncp + c]), r0);
+        const double res = r0 + r1;
+        objc_l += res * res;
+        Rc[i * ncp + c] = T(res);
+        if (!grad_valid) {
+#pragma unroll
+          for (int jj = 0; jj < KH; ++jj)
+            if (jj < k) g[jj] = fma(wi[jj], res, g[jj]);
+        }
+      }
+      if (!grad_valid) {
+        // grad_H = -2 W~^T residc (p/src/rhals.cpp:155)
+#pragma unroll
+        for (int j = 0; j < KH; ++j)
+          if (j < k) {
+            const double gv = -2.0 * g[j];
+            const double gp = Hc[j * ncp + c] > T(0) ? gv : fmin(0.0, gv);
+            pgh_l += gp * gp;
+          }
+      }
+    }
+  }
+
   // S = W~^T W~ (k x k), replicated; invd_j = 1 / max(||W(:,j)||^2 + alpha_h, floor)
   __device__ void compute_s() {
     for (int e = tid; e < k; e += kSwThreads) invd[e] = 1.0 / fmax(wn[e] + a.alpha_h, kDivisionFloor);
@@ -1346,6 +1439,18 @@ struct Sweeper {
     const int sub = lane / LPC, sl = lane % LPC;
     double objc_l = 0.0, pgh_l = 0.0;
     unsigned long long hmask = 0ull;  // rows j of H with a positive entry here (reseed_dead)
+    // lane-per-column path (h_cols_lane) where its k-long fp64 register array fits beside the
+    // kernel's resident Q rows; the warp-per-column path below otherwise
+    constexpr int kHCap = !QS || LREG == 0 ? 64 : LREG <= 32 ? 32 : 0;
+    const int kh = k <= 32 ? 32 : k <= 64 ? 64 : 0;
+    if (kh != 0 && kh <= kHCap && !(a.flags & kHWarpCols)) {
+      if constexpr (kHCap >= 32) {
+        if (kh == 32)
+          h_cols_lane<32>(update, grad_valid, objc_l, pgh_l, hmask);
+        else if constexpr (kHCap >= 64)
+          h_cols_lane<64>(update, grad_valid, objc_l, pgh_l, hmask);
+      }
+    } else
     for (int64_t cb = int64_t(wid) * CPW; cb < NC; cb += int64_t(kSwWarps) * CPW) {
       const int64_t cl = cb + sub;
       const bool valid = cl < NC;
@@ -1954,6 +2059,8 @@ int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t 
   if (std::getenv("RNMF_COL_ORDERED")) a.flags |= kColOrdered;
   // RNMF_XGPU_FLAT: testing knob, the flat cross-GPU column step (every CTA adds into every GPU)
   if (std::getenv("RNMF_XGPU_FLAT")) a.flags |= kXFlat;
+  // RNMF_H_WARP_COLS: testing knob, the warp-per-column H phase
+  if (std::getenv("RNMF_H_WARP_COLS")) a.flags |= kHWarpCols;
   int64_t RM = plan.rows_per_cta, NCM = plan.cols_per_cta;
   void* kargs[] = {&a, const_cast<SmemLayout*>(&L), &RM, &NCM};
   const void* stream64 = nullptr;

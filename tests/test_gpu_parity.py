@@ -247,7 +247,7 @@ def test_fp32_streamed_sweeps_wide(gpu, oracle, k, p, monkeypatch):
     assert_trace_close(res.trace, ref.trace, F32_TRACE_RTOL, F32_FINAL_ATOL)
 
 
-@pytest.mark.parametrize("knobs", [{"RNMF_NO_QREG": "1"}, {"RNMF_FORCE_NOQS": "1"},
+@pytest.mark.parametrize("knobs", [{"RNMF_NO_QREG": "1"}, {"RNMF_FORCE_NOQS": "1"}, {"RNMF_H_WARP_COLS": "1"},
                                    {"RNMF_FORCE_NOQS": "1", "RNMF_NO_QSTREAM": "1"}])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_sweep_kernel_paths(gpu, oracle, knobs, dtype, monkeypatch):
