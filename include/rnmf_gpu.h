@@ -187,6 +187,16 @@ int rnmf_gpu_rhals_fit(rnmf_gpu_context* ctx, const void* x, int dtype, int loca
                        rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len,
                        char* err, size_t err_cap);
 
+/* rnmf::hals_fit (p/include/rnmf/hals.hpp:92, p/src/hals.cpp:268-323): the deterministic
+ * full-space HALS solver, the baseline the reference CLI's `bench` times rHALS against.  Same
+ * arguments and trace semantics as rnmf_gpu_rhals_fit without Omega (every record carries the
+ * full-space metrics; pgrad = pgrad_full, objective_compressed = objective).  UpdateOrder::Grouped
+ * only (ParameterError otherwise); single-GPU contexts. */
+int rnmf_gpu_hals_fit(rnmf_gpu_context* ctx, const void* x, int dtype, int location, int64_t m,
+                      int64_t n, const rnmf_solver_options* opts, const double* w0, const double* h0,
+                      void* w_out, void* h_out, rnmf_trace_record* trace, int64_t trace_cap,
+                      int64_t* trace_len, char* err, size_t err_cap);
+
 /* The sweep / trace loop of rhals_fit (p/src/rhals.cpp:128-213) started from a caller-supplied
  * compressed problem (Q, B, W~, W, H) instead of compress(X).  W~, W, H are in/out.
  * Used for the two-stage parity of rank-deficient inputs. */

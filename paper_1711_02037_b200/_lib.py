@@ -36,6 +36,11 @@ _SIGS = {
         [_vp, _vp, _i32, _i32, _i64, _i64, ctypes.POINTER(SolverOptionsC), _dp, _dp, _dp, _vp, _vp,
          ctypes.POINTER(TraceRecordC), _i64, _i64p, _cp, _sz],
     ),
+    "rnmf_gpu_hals_fit": (
+        _i32,
+        [_vp, _vp, _i32, _i32, _i64, _i64, ctypes.POINTER(SolverOptionsC), _dp, _dp, _vp, _vp,
+         ctypes.POINTER(TraceRecordC), _i64, _i64p, _cp, _sz],
+    ),
     "rnmf_gpu_comm_unique_id": (_i32, [ctypes.c_char_p, _cp, _sz]),
     "rnmf_gpu_context_create_sharded": (_i32, [_i32, _i32, _i32, ctypes.c_char_p, ctypes.POINTER(_vp), _cp, _sz]),
     "rnmf_gpu_rhals_fit_sharded": (

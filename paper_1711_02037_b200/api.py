@@ -330,6 +330,30 @@ def rhals_fit(x, opts: SolverOptions, *, omega=None, w0=None, h0=None, ctx: Opti
     return FitResult(FactorPair(w, h), _trace_list(buf, ln.value))
 
 
+def hals_fit(x, opts: SolverOptions, *, w0=None, h0=None, ctx: Optional[Context] = None) -> FitResult:
+    """rnmf::hals_fit (p/src/hals.cpp:268-323) on the GPU: the deterministic full-space HALS solver
+    (UpdateOrder::Grouped), every sweep recorded with the full-space metrics.  w0 / h0 as in
+    rhals_fit."""
+    X = _Mat(x, name="X")
+    m, n = X.shape
+    c = _ctx_for(X.device or 0, ctx)
+    o = opts.to_c()
+    k = max(int(opts.rank), 0)
+    a0 = _f64_host(w0, m, k, "w0") if w0 is not None else None
+    b0 = _f64_host(h0, k, n, "h0") if h0 is not None else None
+    w = X.empty(m, k)
+    h = X.empty(k, n)
+    cap = max(int(opts.max_iter), 0) + 1
+    buf = (TraceRecordC * cap)()
+    ln = ctypes.c_int64(0)
+    e = err_buffer()
+    _sync_torch(X)
+    st = lib().rnmf_gpu_hals_fit(c.handle, X.ptr, X.dtype_code, X.location, m, n, ctypes.byref(o), _dptr(a0),
+                                 _dptr(b0), _ptr(w), _ptr(h), buf, cap, ctypes.byref(ln), e, _CAP)
+    raise_for_status(st, e)
+    return FitResult(FactorPair(w, h), _trace_list(buf, ln.value))
+
+
 def _sketch_width_nothrow(m, n, k, p):
     bound = min(m, n)
     return max(1, min(k + max(p, 0), bound)) if bound > 0 else 1

@@ -166,6 +166,16 @@ int launch_nndsvd_apply(const T* s, int64_t rows, int l, bool transpose, const d
                         const double* colscale, const double* coef, double fill, T* out, bool out_transposed,
                         cudaStream_t stream);
 
+// ---- deterministic full-space HALS factor updates (kernels_hals.cu) -----------------------------
+// W (m x k) <- clamped_col_update over j with P = X H^T (m x k), G = H H^T (k x k, fp64)
+template <typename T>
+int launch_hals_w_update(T* w, int64_t m, int k, const T* xht, const double* hht, double alpha, double beta,
+                         cudaStream_t st);
+// H (k x n) <- clamped_row_update over j with P = X^T W (n x k), G = W^T W
+template <typename T>
+int launch_hals_h_update(T* h, int64_t n, int k, const T* xtw, const double* wtw, double alpha, double beta,
+                         cudaStream_t st);
+
 // ---- persistent compressed-HALS sweep kernel (kernels_sweeps.cuh) ----------------------------
 enum SweepFlags : int {
   kInitWt = 1,    // W~ <- Q^T W
@@ -251,6 +261,8 @@ struct SweepArgs {
   // launch works in (W is transposed in at the start of the launch and back at the end)
   const float* q4;
   float* wc;
+  // SweepPlan::wide: residc (l x n) in global memory
+  T* rc;
 };
 // q4 (ceil(l_pad / 4) float4 columns of m rows) from row-major Q (m x l); l_pad = SweepPlan::lreg
 int sweep_relayout_q(const float* q, int64_t m, int l, int l_pad, float* q4, cudaStream_t stream);
@@ -274,6 +286,8 @@ struct SweepPlan {
   int qring = 0;  // > 0: streamed slabs through a shared-memory bulk-copy ring of that many stages
   bool f32s = false;  // fp32 X, Q slab not resident: coalesced float4-column Q (SweepArgs::q4), fp32
                       // FMA lift / recompress, column-major W scratch (SweepArgs::wc); lreg = padded l
+  bool wide = false;  // B / H / residc column slabs in global memory (SweepArgs::rc), no P = W~ V in
+                      // shared memory: for n or l x k too large for the shared-memory slabs (C5)
 };
 template <typename T>
 SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_smem);

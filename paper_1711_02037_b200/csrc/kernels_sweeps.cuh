@@ -62,12 +62,18 @@ struct SmemLayout {
   size_t qring, qring_stage, qbars, qring_n;
   // fp32 streamed path: colnew as fp32 (lp floats, zero past l), E as fp32 (l x k) for grad_W
   size_t cnf, ef;
+  // wide: the B / H / residc column slabs stay in global memory (row stride n; H updated in place,
+  // residc in SweepArgs::rc), E is read from the reduction buffer and P = W~ V is not kept --
+  // shared memory independent of n (BASELINE C5: n = 100,000, l = 96, k = 64)
+  bool wide;
 };
 
 constexpr int kQRingMax = 6;  // bulk-copy ring stages (fewer when shared memory is short)
 template <typename T>
-SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring = 0, int f32s_lp = 0) {
+SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring = 0, int f32s_lp = 0,
+                       bool wide = false) {
   SmemLayout L{};
+  L.wide = wide;
   size_t d = 0;
   auto take = [&](size_t count) {  // 16-byte aligned (double2 loads)
     const size_t off = d;
@@ -76,11 +82,11 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring 
   };
   L.wt = take(size_t(l) * (k + 1));
   L.tm = take(size_t(l) * (k + 1));
-  L.em = take(size_t(l) * (k + 1));
+  L.em = wide ? 0 : take(size_t(l) * (k + 1));
   L.vm = take(size_t(k) * k);
   L.sm = take(size_t(k) * k);
   L.wn = take(size_t(k));
-  L.pm = take(size_t(l) * (k + 1));
+  L.pm = wide ? 0 : take(size_t(l) * (k + 1));
   L.colold = take(size_t(l));
   L.colnew = take(size_t(l) > 64 ? size_t(l) : 64);  // zero past l: branch-free padded dot products
   L.invd = take(size_t(k));
@@ -104,9 +110,11 @@ SmemLayout make_layout(int l, int k, int64_t RM, int64_t NCM, bool qs, int ring 
   // the ring and fp32 streamed paths keep the lifted column in registers
   L.wcold = (ring || f32s_lp) ? 0 : takeD(size_t(RM));
   L.wst = qs ? takeT(size_t(k) * RM) : 0;
-  L.bc = takeT(size_t(l) * ncp);
-  L.hc = takeT(size_t(k) * ncp);
-  L.rc = takeT(size_t(l) * ncp);
+  if (!wide) {
+    L.bc = takeT(size_t(l) * ncp);
+    L.hc = takeT(size_t(k) * ncp);
+    L.rc = takeT(size_t(l) * ncp);
+  }
   if (f32s_lp) {
     L.cnf = takeT(size_t(f32s_lp));
     L.ef = takeT(size_t(l) * ((k + 7) & ~7));
@@ -143,6 +151,8 @@ struct Sweeper {
   double *Qs, *wcold;
   T *WsT, *Bc, *Hc, *Rc;
   float *cnf = nullptr, *ef = nullptr;
+  bool wide = false;
+  const double* efin = nullptr;  // wide: E (l x k, row stride k) in the last h_phase reduction buffer
   unsigned epoch = 0;
   int slot = 0;
   unsigned long long* colacc;  // fixed-point column accumulators (3-slot ring)
@@ -189,17 +199,17 @@ struct Sweeper {
     c0 = a.n * g / G;
     NC = a.n * (g + 1) / G - c0;
     RM = RM_;
-    ncp = int(NCM) + 1;
+    ncp = L.wide ? int(a.n) : int(NCM) + 1;
     lq = l + 1;
     kp = k + 1;
     double* D = reinterpret_cast<double*>(smem);
     Wt = D + L.wt;
     Tm = D + L.tm;
-    Em = D + L.em;
+    Em = L.wide ? nullptr : D + L.em;
     Vm = D + L.vm;
     Sm = D + L.sm;
     wn = D + L.wn;
-    Pm = D + L.pm;
+    Pm = L.wide ? nullptr : D + L.pm;
     colold = D + L.colold;
     colnew = D + L.colnew;
     invd = D + L.invd;
@@ -209,9 +219,16 @@ struct Sweeper {
     Qs = QS ? reinterpret_cast<double*>(smem + L.qs) : nullptr;
     wcold = reinterpret_cast<double*>(smem + L.wcold);
     WsT = QS ? reinterpret_cast<T*>(smem + L.wst) : nullptr;
-    Bc = reinterpret_cast<T*>(smem + L.bc);
-    Hc = reinterpret_cast<T*>(smem + L.hc);
-    Rc = reinterpret_cast<T*>(smem + L.rc);
+    if (L.wide) {
+      Bc = const_cast<T*>(a.b) + c0;
+      Hc = a.h + c0;
+      Rc = a.rc + c0;
+    } else {
+      Bc = reinterpret_cast<T*>(smem + L.bc);
+      Hc = reinterpret_cast<T*>(smem + L.hc);
+      Rc = reinterpret_cast<T*>(smem + L.rc);
+    }
+    wide = L.wide;
     if (L.cnf) {
       cnf = reinterpret_cast<float*>(smem + L.cnf);
       ef = reinterpret_cast<float*>(smem + L.ef);
@@ -650,15 +667,17 @@ struct Sweeper {
         WsT[int64_t(j) * RM + r] = a.w[(r0 + r) * k + j];
       }
     }
-    for (int64_t e = tid; e < int64_t(l) * NC; e += kSwThreads) {
-      const int i = int(e / NC);
-      const int64_t cl = e % NC;
-      Bc[i * ncp + cl] = a.b[int64_t(i) * a.n + c0 + cl];
-    }
-    for (int64_t e = tid; e < int64_t(k) * NC; e += kSwThreads) {
-      const int j = int(e / NC);
-      const int64_t cl = e % NC;
-      Hc[j * ncp + cl] = a.h[int64_t(j) * a.n + c0 + cl];
+    if (!wide) {
+      for (int64_t e = tid; e < int64_t(l) * NC; e += kSwThreads) {
+        const int i = int(e / NC);
+        const int64_t cl = e % NC;
+        Bc[i * ncp + cl] = a.b[int64_t(i) * a.n + c0 + cl];
+      }
+      for (int64_t e = tid; e < int64_t(k) * NC; e += kSwThreads) {
+        const int j = int(e / NC);
+        const int64_t cl = e % NC;
+        Hc[j * ncp + cl] = a.h[int64_t(j) * a.n + c0 + cl];
+      }
     }
     if (!(a.flags & kInitWt))
       for (int e = tid; e < l * k; e += kSwThreads) Wt[(e / k) * kp + e % k] = a.wt[e];
@@ -691,7 +710,7 @@ struct Sweeper {
         a.w[(r0 + r) * k + j] = WsT[int64_t(j) * RM + r];
       }
     }
-    if (a.flags & kDoH) {
+    if ((a.flags & kDoH) && !wide) {
       for (int64_t e = tid; e < int64_t(k) * NC; e += kSwThreads) {
         const int j = int(e / NC);
         const int64_t cl = e % NC;
@@ -703,7 +722,7 @@ struct Sweeper {
         const int pe = (e / k) * kp + e % k;
         a.wt[e] = Wt[pe];
         a.tm[e] = Tm[pe];
-        a.em[e] = Em[pe];
+        a.em[e] = Em ? Em[pe] : (efin ? efin[e] : 0.0);
       }
       for (int e = tid; e < k * k; e += kSwThreads) a.vm[e] = Vm[e];
       for (int e = tid; e < k; e += kSwThreads) a.wn[e] = wn[e];
@@ -805,7 +824,7 @@ struct Sweeper {
   // rank-1 update after each column, so the step of column j costs one FMA per entry instead
   // of a k-long dot product (same value as W~ * V(:,j) in rhals_w_component, up to rounding).
   __device__ void compute_p() {
-    for (int e = tid; e < l * k; e += kSwThreads) {
+    for (int e = tid; e < (Pm ? l * k : 0); e += kSwThreads) {
       const int i = e / k, c = e % k;
       const double* wi = Wt + i * kp;
       double s0 = 0.0, s1 = 0.0;
@@ -834,7 +853,23 @@ struct Sweeper {
       double nw = 0.0;
       if (tid < l) {
         const double cur = Wt[tid * kp + j];
-        nw = cur + (Tm[tid * kp + j] - Pm[tid * kp + j] - alpha * cur) * rden;
+        double pij;
+        if (Pm) {
+          pij = Pm[tid * kp + j];
+        } else {  // wide: (W~ V)(i, j) directly
+          const double* wi = Wt + tid * kp;
+          double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+          int c = 0;
+          for (; c + 3 < k; c += 4) {
+            p0 = fma(wi[c], Vm[c * k + j], p0);
+            p1 = fma(wi[c + 1], Vm[(c + 1) * k + j], p1);
+            p2 = fma(wi[c + 2], Vm[(c + 2) * k + j], p2);
+            p3 = fma(wi[c + 3], Vm[(c + 3) * k + j], p3);
+          }
+          for (; c < k; ++c) p0 = fma(wi[c], Vm[c * k + j], p0);
+          pij = (p0 + p1) + (p2 + p3);
+        }
+        nw = cur + (Tm[tid * kp + j] - pij - alpha * cur) * rden;
         colold[tid] = cur;
         colnew[tid] = nw;
         if constexpr (F32S) cnf[tid] = float(nw);
@@ -1227,6 +1262,7 @@ struct Sweeper {
       if (e < l) {
         const double d = v - colold[e];
         Wt[e * kp + j] = v;
+        if (!Pm) return;
         double* pe = Pm + e * kp;
         const double* vj = Vm + j * k;
         int c = 0;
@@ -1276,7 +1312,7 @@ struct Sweeper {
     for (int i = tid; i < l; i += kSwThreads) {
       double s = 0.0;
       for (int c = 0; c < k; ++c) s += Wt[i * kp + c] * Vm[c * k + j];
-      Pm[i * kp + j] = s;
+      if (Pm) Pm[i * kp + j] = s;
     }
     __syncthreads();
     col_prepare(j, true);
@@ -1678,15 +1714,17 @@ struct Sweeper {
       }
     }
     prof_tick(kPfHProducts);
+    efin = fin_base() + lk + kk;  // wide: E stays in this reduction buffer until the next h_phase
     allreduce2(L, [&](int e, double v) {
-      if (e < lk)
+      if (e < lk) {
         Tm[(e / k) * kp + e % k] = v;
-      else if (e < lk + kk)
+      } else if (e < lk + kk) {
         Vm[e - lk] = v;
-      else if (e < 2 * lk + kk)
-        Em[((e - lk - kk) / k) * kp + (e - lk - kk) % k] = v;
-      else
+      } else if (e < 2 * lk + kk) {
+        if (Em) Em[((e - lk - kk) / k) * kp + (e - lk - kk) % k] = v;
+      } else {
         scal[e - (2 * lk + kk)] = v;  // scal[0] = objc, scal[1] = pgh
+      }
     });
     objc = scal[0];
     pgh = scal[1];
@@ -1697,13 +1735,16 @@ struct Sweeper {
   // Thread per row, 16 independent accumulators per pass (throughput- not latency-bound).
   __device__ double pgrad_w() {
     double acc = 0.0;
+    // E = residc H^T: shared memory, or (wide) the last h_phase reduction buffer
+    const double* Ep = Em ? Em : efin;
+    const int es = Em ? kp : k;
     if constexpr (F32S) {
       // fp32: E (fp64, replicated) -> fp32 copy in shared memory; per row the float4 columns of Q,
       // the row's W from the column-major scratch, grad_W(r, j0..j0+7) by fp32 FMA
       const int k8 = (k + 7) & ~7;  // row stride of the fp32 copy: zero pad, 16-byte rows
       for (int e = tid; e < l * k8; e += kSwThreads) {
         const int i = e / k8, j = e % k8;
-        ef[e] = j < k ? float(Em[i * kp + j]) : 0.f;
+        ef[e] = j < k ? float(Ep[i * es + j]) : 0.f;
       }
       __syncthreads();
       constexpr int L4 = LREG / 4;
@@ -1774,7 +1815,7 @@ struct Sweeper {
             for (int i = 0; i < LREG; ++i) {
               if (i < l) {
                 const double qv = double(qf[uu][i]);
-                const double* ei = Em + i * kp + j0;
+                const double* ei = Ep + i * es + j0;
 #pragma unroll
                 for (int t = 0; t < 8; ++t)
                   if (j0 + t < k) sacc[t] += qv * ei[t];
@@ -1801,7 +1842,7 @@ struct Sweeper {
         __syncthreads();
         for (int e = tid; e < l * kE; e += kSwThreads) {
           const int i = e / kE, j = e % kE;
-          red[e] = j < k ? Em[i * kp + j] : 0.0;
+          red[e] = j < k ? Ep[i * es + j] : 0.0;
         }
         __syncthreads();
         if (tid < R) {
@@ -1845,7 +1886,7 @@ struct Sweeper {
         for (int u = 0; u < 16; ++u) sacc[u] = 0.0;
         for (int i = 0; i < l; ++i) {
           const double qv = q(r, i);
-          const double* ei = Em + i * kp + j0;
+          const double* ei = Ep + i * es + j0;
 #pragma unroll
           for (int u = 0; u < 16; ++u)
             if (j0 + u < k) sacc[u] += qv * ei[u];
@@ -2008,30 +2049,41 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
   p.rows_per_cta = ceil_div(m, G);
   p.cols_per_cta = ceil_div(n, G);
   // RNMF_FORCE_NOQS / RNMF_NO_QREG / RNMF_NO_QSTREAM: testing knobs that force the other code paths
-  for (int qs = std::getenv("RNMF_FORCE_NOQS") ? 0 : 1; qs >= 0; --qs) {
-    const SmemLayout L = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, qs != 0);
-    if (L.total <= size_t(max_smem)) {
+  // RNMF_FORCE_WIDE: testing knob, global-memory column slabs even where they fit on chip
+  bool wide = std::getenv("RNMF_FORCE_WIDE") != nullptr;
+  for (int pass = 0; pass < 2 && p.grid == 0; ++pass, wide = true) {
+    for (int qs = (std::getenv("RNMF_FORCE_NOQS") || wide) ? 0 : 1; qs >= 0 && p.grid == 0; --qs) {
+      const SmemLayout L = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, qs != 0, 0, 0, wide);
+      if (qs && L.total > size_t(max_smem)) continue;
       p.q_in_smem = qs != 0;
-      p.smem = L.total;
-      p.grid = G;
-      if (p.q_in_smem && p.rows_per_cta <= kSwThreads && l + 1 <= 64 && !std::getenv("RNMF_NO_QREG"))
-        p.lreg = (l + 1 <= 32) ? 32 : (l + 1 <= 48) ? 48 : 64;
-      if (!p.q_in_smem && sizeof(T) == 4 && !std::getenv("RNMF_NO_QSTREAM") && l <= 96) {
+      p.wide = wide;
+      if (p.q_in_smem) {
+        p.smem = L.total;
+        p.grid = G;
+        if (p.rows_per_cta <= kSwThreads && l + 1 <= 64 && !std::getenv("RNMF_NO_QREG"))
+          p.lreg = (l + 1 <= 32) ? 32 : (l + 1 <= 48) ? 48 : 64;
+        break;
+      }
+      if (sizeof(T) == 4 && !std::getenv("RNMF_NO_QSTREAM") && l <= 96) {
         // fp32 streamed path: float4-column Q, fp32 FMA, column-major W scratch
         const int lp = l <= 32 ? 32 : l <= 64 ? 64 : 96;
-        const SmemLayout LF = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, false, 0, lp);
+        const SmemLayout LF = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, false, 0, lp, wide);
         if (LF.total <= size_t(max_smem)) {
           p.f32s = true;
           p.lreg = lp;
           p.smem = LF.total;
+          p.grid = G;
+          break;
         }
-        return p;
       }
-      if (!p.q_in_smem && !std::getenv("RNMF_NO_QSTREAM") && sizeof(T) == 8 && l + 1 <= 32) {
-        p.lreg = (l + 1 <= 32) ? 32 : 64;
+      if (L.total > size_t(max_smem)) break;  // generic path does not fit either: next pass (wide)
+      p.smem = L.total;
+      p.grid = G;
+      if (!std::getenv("RNMF_NO_QSTREAM") && sizeof(T) == 8 && l + 1 <= 32) {
+        p.lreg = 32;
         // bulk-copy ring for the streamed slab: 16-byte row pitch, the ring must fit as well
         for (int st = kQRingMax; st >= 2 && !p.qring; --st) {
-          const SmemLayout LR = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, false, st);
+          const SmemLayout LR = make_layout<T>(l, k, p.rows_per_cta, p.cols_per_cta, false, st, 0, wide);
           if ((int64_t(l) * int64_t(sizeof(T))) % 16 == 0 && LR.total <= size_t(max_smem) &&
               !std::getenv("RNMF_NO_QRING")) {
             p.qring = st;
@@ -2039,9 +2091,9 @@ SweepPlan plan_sweeps(int64_t m, int64_t n, int l, int k, int sm_count, int max_
           }
         }
       }
-      return p;
     }
   }
+  if (p.grid == 0) p = SweepPlan{};
   return p;
 }
 
@@ -2049,7 +2101,8 @@ template <typename T>
 int launch_sweeps(const SweepArgs<T>& args, const SweepPlan& plan, cudaStream_t stream, bool zero_sync) {
   if (plan.grid <= 0) throw CudaError("sweeps: problem does not fit the persistent kernel");
   const SmemLayout L = make_layout<T>(args.l, args.k, plan.rows_per_cta, plan.cols_per_cta, plan.q_in_smem, plan.qring,
-                                     plan.f32s ? plan.lreg : 0);
+                                     plan.f32s ? plan.lreg : 0, plan.wide);
+  if (plan.wide && args.rc == nullptr) throw CudaError("sweeps: wide layout needs the residc buffer");
   if (plan.f32s && (args.q4 == nullptr || args.wc == nullptr))
     throw CudaError("sweeps: fp32 streamed path needs the q4 / wc buffers");
   if (zero_sync) RNMF_CUDA(cudaMemsetAsync(args.barrier, 0, kSweepSyncBytes, stream));

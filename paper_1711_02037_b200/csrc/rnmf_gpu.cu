@@ -494,6 +494,66 @@ class Engine {
     sumsq_ = ho[1];
   }
 
+  // Y (m x c) = X S in the engine's math mode (the hals_fit W phase's X H^T, p/src/hals.cpp:173).
+  // S is n x c row-major, or (s_rows) given as its c x n transpose -- H itself.
+  void gemm_xs(const T* s, int c, bool s_rows, T* out) {
+    const T* x = x_;
+    const int64_t m = m_, n = n_, ldx = ldx_;
+    if constexpr (std::is_same<T, float>::value) {
+      if (math_ != RNMF_MATH_EXACT) {
+        const bool x3 = math_ == RNMF_MATH_TF32X3;
+        const size_t cap = size_t(tc_npad(c)) * size_t(tc_st_pitch(n));
+        float* sh = ctx_->d<float>("g.st_hi", cap);
+        float* sl = ctx_->d<float>("g.st_lo", cap);
+        tm_.launches += s_rows ? launch_tc_prep_rows(s, c, n, sh, sl, st_) : launch_tc_prep_st(s, n, c, sh, sl, st_, x3);
+        tm_.launches += launch_tc_xw(x, m, n, ldx, sh, sl, c, out, x3, ctx_->sm_count, st_);
+        return;
+      }
+    }
+    const T* sn = s;
+    if (s_rows) {
+      T* st = ctx_->d<T>("g.s_t", size_t(n) * c);
+      tm_.launches += launch_transpose<T>(s, c, n, st, st_);
+      sn = st;
+    }
+    if (sizeof(T) == 4) {
+      T* spad = ctx_->d<T>("g.spad", size_t(xw_tma_spad_len(n, c)));
+      tm_.launches += launch_xw_tma<T>(x, m, n, ldx, sn, c, out, spad, ctx_->sm_count, st_);
+    } else {
+      tm_.launches += launch_xw<T>(x, m, n, ldx, sn, c, out, st_);
+    }
+  }
+
+  // out (n x c) = X^T S, S m x c row-major (the hals_fit H phase's X^T W, p/src/hals.cpp:184).
+  void gemm_xts(const T* s, int c, T* out) {
+    const T* x = x_;
+    const int64_t m = m_, n = n_, ldx = ldx_;
+    if constexpr (std::is_same<T, float>::value) {
+      if (math_ != RNMF_MATH_EXACT) {
+        const bool x3 = math_ == RNMF_MATH_TF32X3;
+        const size_t cap = size_t(tc_npad(c)) * size_t(tc_st_pitch(m));
+        float* sh = ctx_->d<float>("g.st_hi", cap);
+        float* sl = ctx_->d<float>("g.st_lo", cap);
+        const int splits = tc_xtw_splits(m, n, ctx_->sm_count);
+        float* part = ctx_->d<float>("g.part", size_t(splits) * n * c);
+        tm_.launches += launch_tc_prep_st(s, m, c, sh, sl, st_, x3);
+        tm_.launches += launch_tc_xtw(x, m, n, ldx, sh, sl, c, part, splits, x3, ctx_->sm_count, st_);
+        tm_.launches += launch_splitk_reduce<float>(part, splits, n, c, out, false, st_);
+        return;
+      }
+    }
+    if (sizeof(T) == 4) {
+      const int sp = xtw_tma_splits(m, n, ctx_->sm_count);
+      T* part = ctx_->d<T>("g.part2", size_t(sp) * n * c);
+      T* spad = ctx_->d<T>("g.spad2", size_t(xw_tma_spad_len(m, c)));
+      tm_.launches += launch_xtw_tma<T>(x, m, n, ldx, s, c, part, sp, out, false, spad, ctx_->sm_count, st_);
+    } else {
+      const int splits = xtw_default_splits(m, n);
+      T* part = ctx_->d<T>("g.part", size_t(splits) * n * c);
+      tm_.launches += launch_xtw<T>(x, m, n, ldx, s, c, part, splits, out, false, st_);
+    }
+  }
+
   // rqb, p/src/sketch.cpp:52-71 -> Q (m x l), B (l x n) in context buffers.
   // math_mode EXACT: FFMA/DFMA kernels.  TF32 / TF32X3 (fp32 X only): tcgen05 kernels; TF32X3 runs
   // every X pass as 3xTF32 (hi/lo split of both operands, fp32-accurate).
@@ -917,10 +977,12 @@ struct LoopIO {
   bool init_wt;
 };
 
-// fp32 streamed sweep path (SweepPlan::f32s): the float4-column copy of Q (once per Q, i.e. per fit
-// or stage call) and the column-major W scratch.  Returns the kernel launches issued.
+// Sweep-kernel scratch: the fp32 streamed path's float4-column copy of Q (SweepPlan::f32s; once per Q,
+// i.e. per fit or stage call) and column-major W, and the wide layout's residc buffer.  Returns the
+// kernel launches issued.
 template <typename T>
 static int attach_sweep_stream(rnmf_gpu_context* ctx, const SweepPlan& plan, SweepArgs<T>& a, cudaStream_t st) {
+  if (plan.wide) a.rc = ctx->d<T>("sw.rc", size_t(a.l) * size_t(a.n));
   if constexpr (std::is_same<T, float>::value) {
     if (!plan.f32s) return 0;
     float* q4 = ctx->d<float>("sw.q4", size_t(a.m) * size_t(plan.lreg));
@@ -1428,6 +1490,148 @@ static void fit_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int6
   ctx->last.metrics_passes = eng.metrics_passes_;
 }
 
+// hals_fit, p/src/hals.cpp:268-323: the deterministic full-space HALS solver (the reference CLI's
+// `--method hals`, the speed-up baseline of `bench`).  Per sweep (UpdateOrder::Grouped): X H^T
+// (X pass) and H H^T, the row-parallel W update (kernels_hals.cu), X^T W (X pass) and W^T W, the
+// column-parallel H update; every sweep is recorded with the full-space metrics (objective, rel_err,
+// pgrad = pgrad_full, objective_compressed = objective) and tested against the stopping rule.
+template <typename T>
+static void hals_impl(rnmf_gpu_context* ctx, const void* x_in, int location, int64_t m, int64_t n,
+                      const rnmf_solver_options& o, const double* w0, const double* h0, void* w_out, void* h_out,
+                      rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  ctx->last = rnmf_stage_times{};
+  Timer tm(ctx);
+  Engine<T> eng(ctx, tm);
+  eng.set_math(o.math_mode);
+  if (m < 0 || n < 0) throw ShapeError("X has negative dimensions " + shape_string(m, n));
+  const T* x = nullptr;
+  if (m * n > 0) {
+    x = eng.import_x(x_in, location, m, n);
+    eng.scan(true, nullptr);
+  }
+  validate_options_after_data(m, n, o);
+  check_supported(o);
+  if (o.order != RNMF_ORDER_GROUPED)
+    throw ParameterError("B200 path: hals_fit supports UpdateOrder::Grouped");
+  if (trace_cap < o.max_iter + 1)
+    throw ParameterError("trace buffer too small: need " + std::to_string(o.max_iter + 1) + " records, have " +
+                         std::to_string(trace_cap));
+  const int k = int(o.rank);
+  if (k > 64) throw ParameterError("B200 path: rank above 64 is not supported yet");
+  cudaStream_t st = ctx->stream;
+  T* w = ctx->d<T>("w", size_t(m) * k);
+  T* h = ctx->d<T>("h", size_t(k) * n);
+  const bool svd_init = o.init == RNMF_INIT_SVD;
+  if (svd_init && (w0 || h0)) throw ParameterError("init overrides require InitScheme::Random");
+  if (svd_init) {
+    nndsvd_init_dev<T>(ctx, eng, tm, o, m, n, m, w, h);
+  } else {
+    // random_init (p/src/hals.cpp:118-124) from Rng(seed): W then H, scaled by sqrt(mean(X) / k)
+    double* uw = ctx->h<double>("init.uw", size_t(m) * k);
+    double* uh = ctx->h<double>("init.uh", size_t(k) * n);
+    Rng rng(o.seed);
+    if (w0)
+      std::memcpy(uw, w0, sizeof(double) * size_t(m) * k);
+    else
+      fill_uniform(rng, uw, size_t(m) * k);
+    if (h0)
+      std::memcpy(uh, h0, sizeof(double) * size_t(k) * n);
+    else
+      fill_uniform(rng, uh, size_t(k) * n);
+    const double scale = std::sqrt(eng.sum() / double(m * n) / double(k));
+    double* uw_d = ctx->d<double>("init.uw.d", size_t(m) * k);
+    double* uh_d = ctx->d<double>("init.uh.d", size_t(k) * n);
+    tm.span(kH2D, [&] {
+      RNMF_CUDA(cudaMemcpyAsync(uw_d, uw, sizeof(double) * size_t(m) * k, cudaMemcpyHostToDevice, st));
+      RNMF_CUDA(cudaMemcpyAsync(uh_d, uh, sizeof(double) * size_t(k) * n, cudaMemcpyHostToDevice, st));
+    });
+    tm.span(kInit, [&] {
+      tm.launches += launch_scale_cast<T>(uw_d, int64_t(m) * k, scale, w, st);
+      tm.launches += launch_scale_cast<T>(uh_d, int64_t(k) * n, scale, h, st);
+    });
+  }
+  const double x_norm = std::sqrt(eng.sumsq());
+  T* xht = ctx->d<T>("hals.xht", size_t(m) * k);
+  T* xtw = ctx->d<T>("hals.xtw", size_t(n) * k);
+  double* hht = ctx->d<double>("hals.hht", size_t(k) * k);
+  double* wtw = ctx->d<double>("hals.wtw", size_t(k) * k);
+  double* gpart = ctx->d<double>("hals.gpart", size_t(gram_parts(std::max(m, n))) * k * k);
+  double* mres = ctx->d<double>("hals.mres", 2);
+  double* hres = ctx->h<double>("hals.mres.h", 2);
+  Rng reseed_rng = Rng(o.seed).split(kReseedStream);
+
+  int64_t len = 0;
+  auto record = [&](int64_t iter) {
+    eng.metrics(k, w, h, mres);
+    RNMF_CUDA(cudaMemcpyAsync(hres, mres, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RNMF_CUDA(cudaStreamSynchronize(st));
+    rnmf_trace_record& r = trace[len++];
+    r.iter = iter;
+    r.objective = hres[0];
+    r.rel_err = x_norm > 0.0 ? std::sqrt(hres[0]) / x_norm : 0.0;
+    r.pgrad = hres[1];
+    r.pgrad_full = hres[1];
+    r.objective_compressed = hres[0];
+    r.elapsed_s = elapsed();
+  };
+  record(0);
+  const double pgrad0 = trace[0].pgrad;
+  const bool pg_rule = o.stopping == RNMF_STOP_PROJECTED_GRADIENT;
+  const bool stationary = pg_rule && !(pgrad0 > 0.0);
+  std::vector<T> wh, hh;
+  for (int64_t iter = 1; iter <= o.max_iter && !stationary; ++iter) {
+    tm.span(kSweeps, [&] {
+      // W phase (p/src/hals.cpp:172-178)
+      tm.launches += launch_gram_cols<T>(h, k, n, gpart, hht, st);
+      tm.span(kXw, [&] { eng.gemm_xs(h, k, true, xht); });
+      tm.launches += launch_hals_w_update<T>(w, m, k, xht, hht, o.reg.alpha_w, o.reg.beta_w, st);
+      // H phase (p/src/hals.cpp:182-193)
+      tm.span(kXtw, [&] { eng.gemm_xts(w, k, xtw); });
+      tm.launches += launch_gram_rows<T>(w, m, k, gpart, wtw, st);
+      tm.launches += launch_hals_h_update<T>(h, n, k, xtw, wtw, o.reg.alpha_h, o.reg.beta_h, st);
+    });
+    if (o.reseed_dead) {
+      // reseed_dead_components (p/src/hals.cpp:96-105), on the host in the reference's draw order
+      wh.resize(size_t(m) * k);
+      hh.resize(size_t(k) * n);
+      RNMF_CUDA(cudaMemcpyAsync(wh.data(), w, sizeof(T) * wh.size(), cudaMemcpyDeviceToHost, st));
+      RNMF_CUDA(cudaMemcpyAsync(hh.data(), h, sizeof(T) * hh.size(), cudaMemcpyDeviceToHost, st));
+      RNMF_CUDA(cudaStreamSynchronize(st));
+      bool changed = false;
+      for (int j = 0; j < k; ++j) {
+        bool wlive = false, hlive = false;
+        for (int64_t i = 0; i < m && !wlive; ++i) wlive = wh[size_t(i) * k + j] > T(0);
+        if (!wlive) {
+          for (int64_t i = 0; i < m; ++i) wh[size_t(i) * k + j] = T(reseed_rng.uniform() * 1e-4);
+          changed = true;
+        }
+        for (int64_t c = 0; c < n && !hlive; ++c) hlive = hh[size_t(j) * n + c] > T(0);
+        if (!hlive) {
+          for (int64_t c = 0; c < n; ++c) hh[size_t(j) * n + c] = T(reseed_rng.uniform() * 1e-4);
+          changed = true;
+        }
+      }
+      if (changed) {
+        RNMF_CUDA(cudaMemcpyAsync(w, wh.data(), sizeof(T) * wh.size(), cudaMemcpyHostToDevice, st));
+        RNMF_CUDA(cudaMemcpyAsync(h, hh.data(), sizeof(T) * hh.size(), cudaMemcpyHostToDevice, st));
+      }
+    }
+    record(iter);
+    const rnmf_trace_record& last = trace[len - 1];
+    if (pg_rule ? last.pgrad < o.tol * pgrad0 : last.objective < o.tol) break;
+  }
+  *trace_len = len;
+  eng.export_(w_out, location, w, size_t(m) * k);
+  eng.export_(h_out, location, h, size_t(k) * n);
+  RNMF_CUDA(cudaStreamSynchronize(st));
+  tm.finish(ctx->last);
+  ctx->last.sweeps = len - 1;
+  ctx->last.metrics_bytes = eng.metrics_bytes_;
+  ctx->last.metrics_passes = eng.metrics_passes_;
+}
+
 template <typename T>
 static void rqb_impl(rnmf_gpu_context* ctx, const void* a_in, int location, int64_t m, int64_t n, int64_t rank,
                      int64_t p, int64_t qi, int test_matrix, uint64_t seed, const double* omega, int math_mode, void* q_out,
@@ -1878,6 +2082,22 @@ int rnmf_gpu_rhals_fit(rnmf_gpu_context* ctx, const void* x, int dtype, int loca
     else
       fit_impl<double>(ctx, x, location, m, n, *opts, omega, w0, h0, w_out, h_out, trace, trace_cap, trace_len,
                        nullptr, nullptr, nullptr, nullptr, true);
+  });
+}
+
+int rnmf_gpu_hals_fit(rnmf_gpu_context* ctx, const void* x, int dtype, int location, int64_t m, int64_t n,
+                      const rnmf_solver_options* opts, const double* w0, const double* h0, void* w_out, void* h_out,
+                      rnmf_trace_record* trace, int64_t trace_cap, int64_t* trace_len, char* err, size_t err_cap) {
+  return guarded(err, err_cap, [&] {
+    check_ctx(ctx);
+    check_dtype(dtype, location);
+    if (!opts || !trace || !trace_len) throw rnmf_gpu::ParameterError("null options / trace pointer");
+    if (ctx->shard.world > 0) throw rnmf_gpu::ParameterError("hals_fit runs on a single-GPU context");
+    DeviceGuard g(ctx->device);
+    if (dtype == RNMF_F32)
+      hals_impl<float>(ctx, x, location, m, n, *opts, w0, h0, w_out, h_out, trace, trace_cap, trace_len);
+    else
+      hals_impl<double>(ctx, x, location, m, n, *opts, w0, h0, w_out, h_out, trace, trace_cap, trace_len);
   });
 }
 

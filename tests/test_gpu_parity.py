@@ -233,6 +233,22 @@ def test_stage_shape_errors(gpu):
         gpu.rhals_update_H(cp)
 
 
+@pytest.mark.parametrize("mode", ["exact", "tf32x3"])
+def test_c5_shaped_fit(gpu, oracle, mode):
+    """BASELINE C5's solver shape (k = 64, p = 32 -> l = 96, q = 3) on a slice with C5's column count
+    ratio: l x k state and n too large for the shared-memory column slabs, so the sweep kernel runs
+    its wide layout (B / H / residc in global memory, lane-per-column H phase with k = 64) on the
+    fp32 streamed-Q path with l padded to 96; the metrics run the k <= 64 fused pass."""
+    m, n, k, p = 6000, 12000, 64, 32
+    x = oracle.synth_lowrank(m, n, k, 0.05, 77)
+    o = _opts(gpu, rank=k, max_iter=12, tol=1e-300, oversampling=p, power_iterations=3, seed=9)
+    om, w0, h0 = workloads.injected_inputs(8, m, n, k, k + p)
+    ref = oracle.rhals_fit(x, _odict(o), omega=om, w0=w0, h0=h0)
+    o.math_mode = gpu.MathMode.Exact if mode == "exact" else gpu.MathMode.TF32x3
+    res = gpu.rhals_fit(x.astype(np.float32), o, omega=om, w0=w0, h0=h0)
+    assert_trace_close(res.trace, ref.trace, F32_TRACE_RTOL, F32_FINAL_ATOL)
+
+
 @pytest.mark.parametrize("k,p", [(40, 20), (20, 70)])
 def test_fp32_streamed_sweeps_wide(gpu, oracle, k, p, monkeypatch):
     """fp32 streamed-Q sweep path (float4-column Q, fp32 FMA lift / recompress, column-major W
@@ -248,6 +264,7 @@ def test_fp32_streamed_sweeps_wide(gpu, oracle, k, p, monkeypatch):
 
 
 @pytest.mark.parametrize("knobs", [{"RNMF_NO_QREG": "1"}, {"RNMF_FORCE_NOQS": "1"}, {"RNMF_H_WARP_COLS": "1"},
+                                   {"RNMF_FORCE_WIDE": "1"}, {"RNMF_FORCE_WIDE": "1", "RNMF_H_WARP_COLS": "1"},
                                    {"RNMF_FORCE_NOQS": "1", "RNMF_NO_QSTREAM": "1"}])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_sweep_kernel_paths(gpu, oracle, knobs, dtype, monkeypatch):
