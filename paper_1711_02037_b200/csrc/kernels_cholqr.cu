@@ -9,6 +9,9 @@
 // (relative pivot < 1e-12, i.e. A numerically rank deficient, as for BASELINE config 1) or a
 // second-pass R that is not close to I raises a device flag and the caller re-runs TSQR.
 #include "common.cuh"
+
+#include <map>
+#include <mutex>
 #include "kernels.h"
 
 #include <algorithm>
@@ -234,14 +237,31 @@ int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* f
   const size_t csm = size_t(2) * l * (l + 1) * sizeof(double);
   const size_t asm_ = size_t(l) * (l + 1) * sizeof(double) + size_t(64) * (l + 1) * sizeof(double);
   RNMF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream));
-  // per-call attributes: sizes depend on l (chol needs 2 l (l+1) doubles: l <= 112 on B200)
-  RNMF_CUDA(cudaFuncSetAttribute(cq_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
-  RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
-  RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
-  RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(asm_)));
-  RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
-  RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+  // dynamic shared-memory attributes (chol needs 2 l (l+1) doubles: l <= 112 on B200), raised per
+  // device only when a larger l than before arrives (the sizes grow with l); cq_chol_kernel and the
+  // double instantiations are shared by both precisions, so one table covers every kernel
+  {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> done_l;  // (device, sizeof(T)) -> largest l configured
+    int dev = 0;
+    RNMF_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    int& have_t = done_l[{dev, int(sizeof(T))}];
+    int& have_d = done_l[{dev, 0}];  // kernels shared by both precisions
+    if (l > have_t) {
+      RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
+      RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
+      RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+      have_t = l;
+    }
+    if (l > have_d) {
+      RNMF_CUDA(cudaFuncSetAttribute(cq_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
+      RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(asm_)));
+      RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
+      have_d = l;
+    }
+  }
   const int ab = int(std::max<int64_t>(1, std::min<int64_t>(148 * 4, ceil_div(rows, 64))));
   int launches = 0;
   // Gram partials -> (sharded: one local Gram, summed over the GPUs) -> Cholesky -> R^-1

@@ -542,8 +542,9 @@ __global__ void __launch_bounds__(kThreads) gram_cols_kernel(const T* __restrict
 
 // out[e] = sum_p part[p][e]: a block covers 64 entries x 4 part groups (4 independent loads in
 // flight per thread), groups combined in fixed order (deterministic)
-__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* __restrict__ part, int nparts, int len,
-                                                           double* out) {
+// (called in place, out == part, by the CholeskyQR Gram reduction: no __restrict__; each entry is
+// read by its own block before that block writes it)
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const double* part, int nparts, int len, double* out) {
   // 32 entries x 8 part-slices per block; each slice keeps 8 independent loads in flight, the
   // slices are combined in fixed order (deterministic)
   __shared__ double gs[8][33];

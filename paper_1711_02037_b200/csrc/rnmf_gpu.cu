@@ -649,6 +649,13 @@ class Engine {
           if (ar) {
             const double shift = 11.0 * (double(m_total()) * l + double(l) * (l + 1)) * 1.1102230246251565e-16;
             tm_.launches += launch_cholqr2<T>(a, rows, l, out, cqws, cqflag, st_, ar, shift);
+            // the shifted CholeskyQR3 pivots must hold (all GPUs see the same all-reduced Grams):
+            // a Q that is not orthonormal would also void the column reduction's fixed-point bound
+            RNMF_CUDA(cudaMemcpyAsync(hflag, cqflag, sizeof(int), cudaMemcpyDeviceToHost, st_));
+            RNMF_CUDA(cudaStreamSynchronize(st_));
+            if (hflag[0] != 0)
+              throw ParameterError("B200 path: the row-sharded sketch of X is numerically rank deficient "
+                                   "(shifted CholeskyQR3 failed); run it unsharded (Householder TSQR fallback)");
           } else {
             tm_.launches += launch_tsqr<T>(a, rows, l, out, ws, ctx_->max_smem, st_);
           }

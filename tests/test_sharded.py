@@ -200,3 +200,27 @@ def test_sharded_world1_tf32x3(oracle):
             np.testing.assert_allclose(getattr(g, f), o[f], rtol=1e-3, err_msg=f"{f} @ {g.iter}")
             np.testing.assert_allclose(getattr(g, f), getattr(p, f), rtol=1e-6)
     assert abs(res.trace[-1].rel_err - ref.trace[-1]["rel_err"]) < 1e-4
+
+
+@pytest.mark.gpu
+def test_sharded_rank_deficient_sketch(oracle):
+    """BASELINE C1's situation (exact rank 20 < l = 30) on the row-sharded path, whose QR fallback
+    is shifted CholeskyQR3 (Gram-only): either the shifted passes hold and the fit reproduces the
+    final error of the unsharded fit (whose fallback is Householder TSQR), or the library refuses
+    with a ParameterError -- never a silently non-orthonormal Q."""
+    from paper_1711_02037_b200 import api, distributed as d
+    from paper_1711_02037_b200 import workloads
+
+    x = workloads.c1_matrix(0, m=1200, n=600, rank=20)
+    opts = api.SolverOptions(rank=20, oversampling=10, power_iterations=2, max_iter=30, tol=1e-300, seed=0)
+    ctx = d.ShardedContext(0, rank=0, world=1, comm_id=d.comm_unique_id())
+    try:
+        try:
+            res = d.rhals_fit_sharded(x, opts, row_offset=0, m_total=x.shape[0], ctx=ctx)
+        except api.ParameterError as e:
+            assert "rank deficient" in str(e)
+            return
+    finally:
+        ctx.close()
+    plain = api.rhals_fit(x, opts)
+    assert abs(res.trace[-1].rel_err - plain.trace[-1].rel_err) <= 1e-4
