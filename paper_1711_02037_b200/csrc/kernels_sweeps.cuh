@@ -199,17 +199,19 @@ struct Sweeper {
     c0 = a.n * g / G;
     NC = a.n * (g + 1) / G - c0;
     RM = RM_;
-    ncp = L.wide ? int(a.n) : int(NCM) + 1;
+    // (the wide layout never has Q in shared memory: QS variants keep the on-chip slabs statically)
+    const bool wl = !QS && L.wide;
+    ncp = wl ? int(a.n) : int(NCM) + 1;
     lq = l + 1;
     kp = k + 1;
     double* D = reinterpret_cast<double*>(smem);
     Wt = D + L.wt;
     Tm = D + L.tm;
-    Em = L.wide ? nullptr : D + L.em;
+    Em = wl ? nullptr : D + L.em;
     Vm = D + L.vm;
     Sm = D + L.sm;
     wn = D + L.wn;
-    Pm = L.wide ? nullptr : D + L.pm;
+    Pm = wl ? nullptr : D + L.pm;
     colold = D + L.colold;
     colnew = D + L.colnew;
     invd = D + L.invd;
@@ -219,7 +221,7 @@ struct Sweeper {
     Qs = QS ? reinterpret_cast<double*>(smem + L.qs) : nullptr;
     wcold = reinterpret_cast<double*>(smem + L.wcold);
     WsT = QS ? reinterpret_cast<T*>(smem + L.wst) : nullptr;
-    if (L.wide) {
+    if (wl) {
       Bc = const_cast<T*>(a.b) + c0;
       Hc = a.h + c0;
       Rc = a.rc + c0;
@@ -228,7 +230,7 @@ struct Sweeper {
       Hc = reinterpret_cast<T*>(smem + L.hc);
       Rc = reinterpret_cast<T*>(smem + L.rc);
     }
-    wide = L.wide;
+    wide = wl;
     if (L.cnf) {
       cnf = reinterpret_cast<float*>(smem + L.cnf);
       ef = reinterpret_cast<float*>(smem + L.ef);
@@ -854,7 +856,7 @@ struct Sweeper {
       if (tid < l) {
         const double cur = Wt[tid * kp + j];
         double pij;
-        if (Pm) {
+        if (QS || Pm) {  // (the wide layout, Pm == nullptr, never has Q in shared memory)
           pij = Pm[tid * kp + j];
         } else {  // wide: (W~ V)(i, j) directly
           const double* wi = Wt + tid * kp;
@@ -1262,7 +1264,9 @@ struct Sweeper {
       if (e < l) {
         const double d = v - colold[e];
         Wt[e * kp + j] = v;
-        if (!Pm) return;
+        if constexpr (!QS) {
+          if (!Pm) return;
+        }
         double* pe = Pm + e * kp;
         const double* vj = Vm + j * k;
         int c = 0;
@@ -1721,7 +1725,7 @@ struct Sweeper {
       } else if (e < lk + kk) {
         Vm[e - lk] = v;
       } else if (e < 2 * lk + kk) {
-        if (Em) Em[((e - lk - kk) / k) * kp + (e - lk - kk) % k] = v;
+        if (QS || Em) Em[((e - lk - kk) / k) * kp + (e - lk - kk) % k] = v;
       } else {
         scal[e - (2 * lk + kk)] = v;  // scal[0] = objc, scal[1] = pgh
       }
@@ -1736,8 +1740,8 @@ struct Sweeper {
   __device__ double pgrad_w() {
     double acc = 0.0;
     // E = residc H^T: shared memory, or (wide) the last h_phase reduction buffer
-    const double* Ep = Em ? Em : efin;
-    const int es = Em ? kp : k;
+    const double* Ep = (QS || Em) ? Em : efin;
+    const int es = (QS || Em) ? kp : k;
     if constexpr (F32S) {
       // fp32: E (fp64, replicated) -> fp32 copy in shared memory; per row the float4 columns of Q,
       // the row's W from the column-major scratch, grad_W(r, j0..j0+7) by fp32 FMA

@@ -1214,11 +1214,14 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          // raw H and H^T slabs only; the split warps write their lo slabs on chip
-          tc::mbar_arrive_expect_tx(&full[s], uint32_t(kXTileBytes + C::kSBytes + 4096));
+          // X and the H / H^T slabs with their lo parts (prepared once per evaluation): the split
+          // warps, the busiest role of this kernel, only split X
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
           tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
           tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
+          tc::tma_load_2d(shi(s) + C::kSBytes, &tmSlo, &full[s], kc * kBK, 0);
           tc::tma_load_2d(htp(s), &tmHhi, &full[s], 0, kc * kBK);
+          tc::tma_load_2d(htp(s) + 4096, &tmHlo, &full[s], 0, kc * kBK);
         }
       }
     }
@@ -1278,8 +1281,6 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
         tc::mbar_wait(&full[s], (it / S) & 1);
         tc::mbar_wait(&loempty[j], ((it / kLoSlots) & 1) ^ 1);
         split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(xst(s)), reinterpret_cast<float4*>(lo(j)), st);
-        split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(shi(s)), reinterpret_cast<float4*>(shi(s) + C::kSBytes), st);
-        split_lo_tile<256>(reinterpret_cast<const float4*>(htp(s)), reinterpret_cast<float4*>(htp(s) + 4096), st);
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&lofull[j]);
       }
@@ -1475,12 +1476,16 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          // raw H and H^T slabs only; the split warps write their lo slabs on chip
-          tc::mbar_arrive_expect_tx(&full[s], uint32_t(kXTileBytes + C::kSBytes + 2 * 4096));
+          // X and the H / H^T slabs with their lo parts: the split warps only split X
+          tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
           tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
           tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
+          tc::tma_load_2d(shi(s) + C::kSBytes, &tmSlo, &full[s], kc * kBK, 0);
 #pragma unroll
-          for (int a = 0; a < 2; ++a) tc::tma_load_2d(htp(s) + a * 8192, &tmHhi, &full[s], a * 32, kc * kBK);
+          for (int a = 0; a < 2; ++a) {
+            tc::tma_load_2d(htp(s) + a * 8192, &tmHhi, &full[s], a * 32, kc * kBK);
+            tc::tma_load_2d(htp(s) + a * 8192 + 4096, &tmHlo, &full[s], a * 32, kc * kBK);
+          }
         }
       }
     }
@@ -1536,10 +1541,6 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
         tc::mbar_wait(&full[s], (it / S) & 1);
         tc::mbar_wait(&loempty[j], ((it / LO) & 1) ^ 1);
         split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(xst(s)), reinterpret_cast<float4*>(lo(j)), st);
-        split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(shi(s)), reinterpret_cast<float4*>(shi(s) + C::kSBytes), st);
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-          split_lo_tile<256>(reinterpret_cast<const float4*>(htp(s) + a * 8192), reinterpret_cast<float4*>(htp(s) + a * 8192 + 4096), st);
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&lofull[j]);
       }
