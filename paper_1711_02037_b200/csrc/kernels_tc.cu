@@ -94,25 +94,38 @@ __device__ __forceinline__ void split_lo_tile(const float4* __restrict__ x4, flo
 // two slabs adjacent so that X_hi * [S_hi; S_lo]^T is ONE UMMA with N = 2 NPAD.  3xTF32 keeps the
 // lo X tiles in a separate 3-slot ring so the TMA ring stays deep.  TMEM accumulator buffer =
 // [X_hi S_hi | X_hi S_lo + X_lo S_hi] (2 NPAD columns; NPAD for 1xTF32), double-buffered.
-template <int NPAD, bool X3>
+// LT (3xTF32 only): the lo X tile lives in TENSOR MEMORY instead of shared memory -- the split warps
+// read their rows of the X stage, write lo with tcgen05.st into 32 TMEM columns per ring stage, and
+// the small-term UMMA takes A from TMEM.  That removes the lo tile's shared-memory write and its
+// UMMA operand read (ncu: the shared-memory data pipe, LSU + tensor-core wavefronts, was ~100 % busy
+// with the lo ring in shared memory), and frees 48 KB for a deeper TMA ring.  The S^T lo slab comes
+// by TMA from the prepared global copy.
+template <int NPAD, bool X3, bool LT = false>
 struct TcCfg {
+  static_assert(!LT || X3, "LT is a 3xTF32 layout");
   static constexpr int kSBytes = NPAD * kBK * 4;  // one S^T slab (NPAD rows x 128 B)
   static constexpr int kStageBytes = kXTileBytes + kSBytes * (X3 ? 2 : 1);
-  static constexpr int kLoBytes = X3 ? kLoSlots * kXTileBytes : 0;
+  static constexpr int kLoBytes = (X3 && !LT) ? kLoSlots * kXTileBytes : 0;
   static constexpr int kStages = std::min(8, (kSmemBudget - kLoBytes - 2048) / kStageBytes);
+  // LT: TMEM lo slot s belongs to ring stage s and is released with it (one commit per stage)
+  static constexpr int kLoN = LT ? kStages : kLoSlots;
   static constexpr int kAccCols = X3 ? 2 * NPAD : NPAD;
-  static constexpr int kAccBufs = (2 * kAccCols <= 512) ? 2 : 1;
-  static constexpr int kUsedCols = kAccBufs * kAccCols;
+  static constexpr int kLoCols = LT ? kLoN * kBK : 0;
+  static constexpr int kAccBufs = (2 * kAccCols + kLoCols <= 512) ? 2 : 1;
+  static constexpr int kLoBase = kAccBufs * kAccCols;  // first TMEM column of the lo ring
+  static constexpr int kUsedCols = kAccBufs * kAccCols + kLoCols;
   static constexpr int kTmemCols = kUsedCols <= 32 ? 32 : kUsedCols <= 64 ? 64 : kUsedCols <= 128 ? 128
                                    : kUsedCols <= 256 ? 256 : 512;
+  static constexpr int kThreads = LT ? 448 : X3 ? kTcThreadsX3 : kTcThreads;
+  static constexpr int kSplit = LT ? 256 : kSplitThreads;  // lo-producing threads
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kLoBytes + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(kStages >= 2, "ring too shallow");
   static_assert(kUsedCols <= 512, "TMEM");
 };
 
-template <int NPAD, bool X3>
+template <int NPAD, bool X3, bool LT = false>
 struct TcSmem {
-  using C = TcCfg<NPAD, X3>;
+  using C = TcCfg<NPAD, X3, LT>;
   unsigned char* base;
   uint64_t *full, *empty, *lofull, *loempty, *tfull, *tempty;
   uint32_t* tmem_slot;
@@ -122,8 +135,8 @@ struct TcSmem {
     full = bars;
     empty = full + C::kStages;
     lofull = empty + C::kStages;
-    loempty = lofull + kLoSlots;
-    tfull = loempty + kLoSlots;
+    loempty = lofull + C::kLoN;
+    tfull = loempty + C::kLoN;
     tempty = tfull + 2;
     tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   }
@@ -131,13 +144,13 @@ struct TcSmem {
   __device__ unsigned char* shi(int s) const { return x(s) + kXTileBytes; }
   __device__ unsigned char* slo(int s) const { return shi(s) + C::kSBytes; }
   __device__ unsigned char* lo(int j) const { return base + size_t(C::kStages) * C::kStageBytes + size_t(j) * kXTileBytes; }
-  __device__ void init(int split_count) const {
+  __device__ void init() const {
     for (int s = 0; s < C::kStages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    for (int j = 0; j < kLoSlots; ++j) {
-      tc::mbar_init(&lofull[j], split_count);
+    for (int j = 0; j < C::kLoN; ++j) {
+      tc::mbar_init(&lofull[j], LT ? C::kSplit / 32 : C::kSplit);
       tc::mbar_init(&loempty[j], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -148,20 +161,58 @@ struct TcSmem {
   }
 };
 
+#ifdef RNMF_TC_PROF
+// (development) cycles CTA 0's roles spend waiting / working in tc_xw_kernel<LT>, read by tools
+__device__ long long g_tc_prof[16];
+#define TCP_T0() const long long tcp_t0 = clock64()
+#define TCP_ADD(slot) do { tcp_acc[slot] += clock64() - tcp_t0; } while (0)
+#define TCP_DECL() long long tcp_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}
+#define TCP_FLUSH() do { if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64 || threadIdx.x == 128)) for (int i = 0; i < 9; ++i) if (tcp_acc[i]) atomicAdd(reinterpret_cast<unsigned long long*>(&g_tc_prof[i]), (unsigned long long)tcp_acc[i]); } while (0)
+#else
+#define TCP_T0() do { } while (0)
+#define TCP_ADD(slot) do { } while (0)
+#define TCP_DECL() do { } while (0)
+#define TCP_FLUSH() do { } while (0)
+#endif
+
+// LT split warps: 2, 3 and 8..13 -- two warps per TMEM lane quadrant (warp % 4), the first of a
+// pair taking K columns 0..15 of the stage and the second 16..31.
+__device__ __forceinline__ int lt_half(int warp) { return (warp == 2 || warp == 3 || warp == 8 || warp == 9) ? 0 : 1; }
+
+// lo of 16 K values of one A row -> TMEM (lane = A row, 16 columns from taddr)
+__device__ __forceinline__ void lt_store16(uint32_t taddr, const uint32_t (&v)[16]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r[i] = tf32_lo_bits(v[i]);
+  tc::tmem_st_32x32b_x16(taddr, r);
+  tc::tmem_st_wait();
+  tc::tc_fence_before();
+}
+
 // One K stage of UMMAs into accumulator buffer d.  a_desc(k, base) builds the A descriptor of
 // k-step k (A = X tile hi or lo); B is K-major SW128 in either kernel.
-template <int NPAD, bool X3, bool A_MN, typename ADesc>
+template <int NPAD, bool X3, bool A_MN, bool LT = false, typename ADesc>
 __device__ __forceinline__ void issue_stage(uint32_t d, uint32_t xa, uint32_t la, uint32_t ba, bool fresh, ADesc a_desc) {
   constexpr uint32_t idesc1 = tc::make_idesc_tf32(NPAD, A_MN, false);
   constexpr uint32_t idesc2 = tc::make_idesc_tf32(2 * NPAD, A_MN, false);
+  constexpr uint32_t idesc_ts = tc::make_idesc_tf32(NPAD, false, false);  // A from TMEM (la = TMEM address)
 #pragma unroll
   for (int k = 0; k < kBK / 8; ++k) {
     const uint64_t adesc = a_desc(xa, k);
     const uint64_t bdesc = tc::make_sdesc(ba + k * 32, 16, 1024);
     const uint32_t acc = (fresh && k == 0) ? 0u : 1u;
     if (X3) {
+#ifdef RNMF_TC_DBG_NOSLO  // (experiment) hi MMA without the S_lo half
+      tc::umma_tf32(d, adesc, bdesc, idesc1, acc);
+#else
       tc::umma_tf32(d, adesc, bdesc, idesc2, acc);                                 // X_hi [S_hi; S_lo]
-      tc::umma_tf32(d + NPAD, a_desc(la, k), bdesc, idesc1, 1u);                   // += X_lo S_hi (small terms)
+#endif
+#ifndef RNMF_TC_DBG_NOLOMMA
+      if (LT)
+        tc::umma_tf32_ts(d + NPAD, la + uint32_t(k * 8), bdesc, idesc_ts, 1u);     // += X_lo S_hi, A in TMEM
+      else
+        tc::umma_tf32(d + NPAD, a_desc(la, k), bdesc, idesc1, 1u);                 // += X_lo S_hi (small terms)
+#endif
     } else {
       tc::umma_tf32(d, adesc, bdesc, idesc1, acc);
     }
@@ -170,9 +221,9 @@ __device__ __forceinline__ void issue_stage(uint32_t d, uint32_t xa, uint32_t la
 
 // Epilogue: add one accumulator buffer (this warp's 32 lanes) into the fp32 registers a[]:
 // a += hihi + small, each add rounded to nearest.
-template <int NPAD, bool X3>
+template <int NPAD, bool X3, bool WIDE = true>
 __device__ __forceinline__ void drain_acc(uint32_t taddr, float (&a)[NPAD]) {
-  if constexpr (X3 && NPAD % 32 == 0) {
+  if constexpr (X3 && NPAD % 32 == 0 && WIDE) {
     // 32-column loads of both halves, one wait per 32 columns
 #pragma unroll
     for (int cc = 0; cc < NPAD / 32; ++cc) {
@@ -216,20 +267,21 @@ struct XwParams {
 // The K loop is cut into chunks of p.chunk stages; each chunk starts a fresh TMEM accumulator that
 // the epilogue adds into fp32 registers, so the tensor core's truncating accumulation never runs
 // over more than p.chunk * 32 terms (tools/sketch_acc.cu measures the effect).
-template <int NPAD, bool X3>
-__global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid_constant__ CUtensorMap tmX,
+template <int NPAD, bool X3, bool LT>
+__global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xw_kernel(const __grid_constant__ CUtensorMap tmX,
                                                                     const __grid_constant__ CUtensorMap tmShi,
                                                                     const __grid_constant__ CUtensorMap tmSlo, XwParams p) {
-  using C = TcCfg<NPAD, X3>;
+  using C = TcCfg<NPAD, X3, LT>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const TcSmem<NPAD, X3> sm(smem_raw);
+  const TcSmem<NPAD, X3, LT> sm(smem_raw);
+  TCP_DECL();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = ceil_div(p.m, kBM);
   const int nk = int(ceil_div(p.n, kBK));
 
   if (threadIdx.x == 0) {
-    sm.init(kSplitThreads);
+    sm.init();
     tc::tma_prefetch(&tmX);
     tc::tma_prefetch(&tmShi);
     if (X3) tc::tma_prefetch(&tmSlo);
@@ -244,20 +296,80 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
     // ---------------- TMA producer
     if (tc::elect_one()) {
       uint32_t it = 0;
-      // 3xTF32: only the raw S^T slab comes from L2; the split warps write its lo slab on chip
-      const uint32_t bytes = uint32_t(kXTileBytes + C::kSBytes);
+      // 3xTF32: only the raw S^T slab comes from L2 and the split warps write its lo slab on chip;
+      // LT: the split warps only handle X, the lo slab comes by TMA
+      const uint32_t bytes = uint32_t(kXTileBytes + C::kSBytes * (LT ? 2 : 1));
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
-          tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
+          { TCP_T0(); tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1); TCP_ADD(0); }
+#ifdef RNMF_TC_DBG_NOSLOAD  // (experiment) the S slab only on the first pass over the ring
+          if (it >= uint32_t(S)) {
+            tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes));
+            tc::tma_load_2d(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM));
+            continue;
+          }
+#endif
           tc::mbar_arrive_expect_tx(&sm.full[s], bytes);
           tc::tma_load_2d(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM));
           tc::tma_load_2d(sm.shi(s), &tmShi, &sm.full[s], kc * kBK, 0);
+          if (LT) tc::tma_load_2d(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- UMMA issuer
+    if constexpr (LT) {
+      // descriptors as {lo, hi} words advanced by adds (no make_sdesc per K step), no integer
+      // divisions in the loop; the stage's single commit releases the X / S stage and its TMEM lo
+      // slot together.  The whole warp runs the loop and one elected lane issues (an `if (lane == 0)`
+      // loop makes the compiler wrap every UTCHMMA in an election loop).
+      constexpr uint32_t kHi = tc::sdesc_hi(1024, tc::kLayoutSW128);
+      constexpr uint32_t idesc2 = tc::make_idesc_tf32(2 * NPAD, false, false);
+      constexpr uint32_t idesc_ts = tc::make_idesc_tf32(NPAD, false, false);
+      const uint32_t x0 = (tc::smem_u32(sm.x(0)) >> 4) + tc::sdesc_lo_const(16);
+      uint32_t ci = 0, s = 0, ph = 0;
+      uint32_t d = tmem_base;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int kin = 0;
+        for (int kc = 0; kc < nk; ++kc) {
+          const bool cend = (kin == p.chunk - 1) || (kc == nk - 1);
+          const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+          if (kin == 0) {
+            TCP_T0();
+            tc::mbar_wait(&sm.tempty[acc], ((C::kAccBufs == 2 ? ci >> 1 : ci) & 1) ^ 1);
+            TCP_ADD(1);
+            d = tmem_base + uint32_t(acc * C::kAccCols);
+          }
+          { TCP_T0(); tc::mbar_wait(&sm.full[s], ph); TCP_ADD(2); }
+          { TCP_T0(); tc::mbar_wait(&sm.lofull[s], ph); TCP_ADD(3); }
+          tc::tc_fence_after();
+          TCP_T0();
+          if (tc::elect_one()) {
+            const uint32_t xa = x0 + s * uint32_t(C::kStageBytes >> 4), ba = xa + uint32_t(kXTileBytes >> 4);
+            const uint32_t la = tmem_base + uint32_t(C::kLoBase) + s * uint32_t(kBK);
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k) {
+              tc::umma_tf32_w(d, xa + 2 * k, kHi, ba + 2 * k, kHi, idesc2, (kin == 0 && k == 0) ? 0u : 1u);
+#ifndef RNMF_TC_DBG_NOLOMMA
+              tc::umma_tf32_ts_w(d + NPAD, la + 8 * k, ba + 2 * k, kHi, idesc_ts, 1u);
+#endif
+            }
+            tc::umma_commit(&sm.empty[s]);
+            if (cend) tc::umma_commit(&sm.tfull[acc]);
+          }
+          __syncwarp();
+          if (cend) {
+            ++ci;
+            kin = 0;
+          } else {
+            ++kin;
+          }
+          if (++s == uint32_t(S)) s = 0, ph ^= 1;
+          TCP_ADD(4);
+        }
+      }
+    } else {
     uint32_t it = 0, ci = 0;
     uint32_t d = tmem_base;
     auto adesc = [](uint32_t base, int k) { return tc::make_sdesc(base + k * 32, 16, 1024); };
@@ -286,9 +398,43 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
         __syncwarp();
       }
     }
+    }
   } else if (warp < 4 || warp >= 8) {
-    // ---------------- 3xTF32 split warps: lo tiles into their own ring
-    if (X3) {
+    // ---------------- 3xTF32 split warps
+    if constexpr (LT) {
+      // lo of this thread's X row (16 of the stage's 32 K values) -> the TMEM lo ring
+      const int quad = warp & 3, r = quad * 32 + lane, half = lt_half(warp);
+      const uint32_t lane_off = uint32_t(quad * 32) << 16;
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          // full[s] of this pass implies the UMMAs that read TMEM lo slot s a ring ago are done (the
+          // producer refilled the stage only after their commit)
+          const int s = int(it % S);
+          {  // one lane polls the barrier for its warp
+            TCP_T0();
+            if (lane == 0) tc::mbar_wait(&sm.full[s], (it / S) & 1);
+            __syncwarp();
+            TCP_ADD(5);
+          }
+          TCP_T0();
+          const uint32_t xrow = tc::smem_u32(sm.x(s)) + uint32_t(r) * 128u;
+          uint32_t v[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)  // 16-byte chunk 4 half + c of the row, 128 B swizzle
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[4 * c]), "=r"(v[4 * c + 1]), "=r"(v[4 * c + 2]), "=r"(v[4 * c + 3])
+                         : "r"(xrow + uint32_t(((4 * half + c) ^ (r & 7)) * 16)) : "memory");
+          tc::tc_fence_after();
+#ifndef RNMF_TC_DBG_NOSPLIT
+          lt_store16(tmem_base + lane_off + uint32_t(C::kLoBase + s * kBK + half * 16), v);
+#endif
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sm.lofull[s]);
+          TCP_ADD(6);
+        }
+      }
+    } else if (X3) {  // lo tiles into their own shared-memory ring
       const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;  // 0..191
       uint32_t it = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -296,8 +442,10 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
           const int s = int(it % S), j = int(it % kLoSlots);
           tc::mbar_wait(&sm.full[s], (it / S) & 1);
           tc::mbar_wait(&sm.loempty[j], ((it / kLoSlots) & 1) ^ 1);
+#ifndef RNMF_TC_DBG_NOSPLIT
           split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(sm.x(s)), reinterpret_cast<float4*>(sm.lo(j)), st);
           split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(sm.shi(s)), reinterpret_cast<float4*>(sm.slo(s)), st);
+#endif
           tc::fence_proxy_async_smem();
           tc::mbar_arrive(&sm.lofull[j]);
         }
@@ -315,11 +463,13 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
       for (int q = 0; q < NPAD; ++q) a[q] = 0.f;
       for (int ch = 0; ch < nch; ++ch, ++ci) {
         const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
-        tc::mbar_wait(&sm.tfull[acc], (C::kAccBufs == 2 ? ci >> 1 : ci) & 1);
+        { TCP_T0(); tc::mbar_wait(&sm.tfull[acc], (C::kAccBufs == 2 ? ci >> 1 : ci) & 1); TCP_ADD(7); }
+        TCP_T0();
         tc::tc_fence_after();
-        drain_acc<NPAD, X3>(tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * C::kAccCols), a);
+        drain_acc<NPAD, X3, !(LT && NPAD > 48)>(tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * C::kAccCols), a);
         tc::tc_fence_before();
         tc::mbar_arrive(&sm.tempty[acc]);
+        TCP_ADD(8);
       }
       if (row < p.m) {
 #pragma unroll
@@ -328,6 +478,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xw_kernel(const __grid
       }
     }
   }
+  TCP_FLUSH();
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -350,20 +501,20 @@ struct XtwParams {
   int chunk;    // K stages (32 rows each) per TMEM accumulation chunk
 };
 
-template <int NPAD, bool X3>
-__global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __grid_constant__ CUtensorMap tmX,
+template <int NPAD, bool X3, bool LT>
+__global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_kernel(const __grid_constant__ CUtensorMap tmX,
                                                                      const __grid_constant__ CUtensorMap tmSt,
                                                                      const __grid_constant__ CUtensorMap tmStLo, XtwParams p) {
-  using C = TcCfg<NPAD, X3>;
+  using C = TcCfg<NPAD, X3, LT>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const TcSmem<NPAD, X3> sm(smem_raw);
+  const TcSmem<NPAD, X3, LT> sm(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ctiles = ceil_div(p.n, 128);
   const int64_t units = ctiles * p.splits;
 
   if (threadIdx.x == 0) {
-    sm.init(kSplitThreads);
+    sm.init();
     tc::tma_prefetch(&tmX);
     tc::tma_prefetch(&tmSt);
     if (X3) tc::tma_prefetch(&tmStLo);
@@ -393,14 +544,70 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
           const int s = int(it % S);
           tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
           // 3xTF32: the raw S^T slab only; its lo slab is written on chip by the split warps
-          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes + C::kSBytes));
+          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes + C::kSBytes * (LT ? 2 : 1)));
 #pragma unroll
           for (int b = 0; b < 4; ++b) tc::tma_load_2d(sm.x(s) + b * 4096, &tmX, &sm.full[s], int(ct * 128 + b * 32), int(r));
           tc::tma_load_2d(sm.shi(s), &tmSt, &sm.full[s], int(r), 0);
+          if (LT) tc::tma_load_2d(sm.slo(s), &tmStLo, &sm.full[s], int(r), 0);
         }
       }
     }
   } else if (warp == 1) {
+    if constexpr (LT) {
+      constexpr uint32_t kAHi = tc::sdesc_hi(512, tc::kLayoutSW128Base32B);  // MN-major A: SBO 512 B per 4 rows
+      constexpr uint32_t kBHi = tc::sdesc_hi(1024, tc::kLayoutSW128);
+      constexpr uint32_t idesc2 = tc::make_idesc_tf32(2 * NPAD, true, false);
+      constexpr uint32_t idesc_ts = tc::make_idesc_tf32(NPAD, false, false);
+      const uint32_t a0 = (tc::smem_u32(sm.x(0)) >> 4) + tc::sdesc_lo_const(4096);  // LBO 4 KB between boxes
+      const uint32_t b0 = (tc::smem_u32(sm.shi(0)) >> 4) + tc::sdesc_lo_const(16);
+      uint32_t ci = 0, s = 0, ph = 0;
+      uint32_t d = tmem_base;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t r0, r1;
+        unit_rows(u, r0, r1);
+        if (r0 >= r1) {  // empty split: still hand an (all-zero) chunk to the epilogue
+          const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+          tc::mbar_wait(&sm.tempty[acc], ((C::kAccBufs == 2 ? ci >> 1 : ci) & 1) ^ 1);
+          if (tc::elect_one()) tc::mbar_arrive(&sm.tfull[acc]);
+          ++ci;
+          __syncwarp();
+          continue;
+        }
+        int kin = 0;
+        for (int64_t r = r0; r < r1; r += kBK) {
+          const bool cend = (kin == p.chunk - 1) || (r + kBK >= r1);
+          const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
+          if (kin == 0) {
+            tc::mbar_wait(&sm.tempty[acc], ((C::kAccBufs == 2 ? ci >> 1 : ci) & 1) ^ 1);
+            d = tmem_base + uint32_t(acc * C::kAccCols);
+          }
+          tc::mbar_wait(&sm.full[s], ph);
+          tc::mbar_wait(&sm.lofull[s], ph);
+          tc::tc_fence_after();
+          if (tc::elect_one()) {
+            const uint32_t xa = a0 + s * uint32_t(C::kStageBytes >> 4), ba = b0 + s * uint32_t(C::kStageBytes >> 4);
+            const uint32_t la = tmem_base + uint32_t(C::kLoBase) + s * uint32_t(kBK);
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k) {
+              tc::umma_tf32_w(d, xa + 64 * k, kAHi, ba + 2 * k, kBHi, idesc2, (kin == 0 && k == 0) ? 0u : 1u);
+#ifndef RNMF_TC_DBG_NOLOMMA
+              tc::umma_tf32_ts_w(d + NPAD, la + 8 * k, ba + 2 * k, kBHi, idesc_ts, 1u);
+#endif
+            }
+            tc::umma_commit(&sm.empty[s]);
+            if (cend) tc::umma_commit(&sm.tfull[acc]);
+          }
+          __syncwarp();
+          if (cend) {
+            ++ci;
+            kin = 0;
+          } else {
+            ++kin;
+          }
+          if (++s == uint32_t(S)) s = 0, ph ^= 1;
+        }
+      }
+    } else {
     uint32_t it = 0, ci = 0;
     uint32_t d = tmem_base;
     // MN-major A (SW128_BASE32B): LBO = 4 KB between 32-column boxes, SBO = 512 B per 4 rows
@@ -425,13 +632,14 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
           tc::tc_fence_after();
           d = tmem_base + uint32_t(acc * C::kAccCols);
         }
-        const int s = int(it % S), j = int(it % kLoSlots);
+        const int s = int(it % S), j = int(it % C::kLoN);
         tc::mbar_wait(&sm.full[s], (it / S) & 1);
-        if (X3) tc::mbar_wait(&sm.lofull[j], (it / kLoSlots) & 1);
+        if (X3) tc::mbar_wait(&sm.lofull[j], (it / C::kLoN) & 1);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          issue_stage<NPAD, X3, true>(d, tc::smem_u32(sm.x(s)), tc::smem_u32(sm.lo(j)), tc::smem_u32(sm.shi(s)),
-                                      kin == 0, adesc);
+          issue_stage<NPAD, X3, true, LT>(d, tc::smem_u32(sm.x(s)),
+                                          LT ? tmem_base + uint32_t(C::kLoBase + j * kBK) : tc::smem_u32(sm.lo(j)),
+                                          tc::smem_u32(sm.shi(s)), kin == 0, adesc);
           tc::umma_commit(&sm.empty[s]);
           if (X3) tc::umma_commit(&sm.loempty[j]);
           if (cend) tc::umma_commit(&sm.tfull[acc]);
@@ -445,8 +653,39 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
         __syncwarp();
       }
     }
+    }
   } else if (warp < 4 || warp >= 8) {
-    if (X3) {  // 3xTF32 lo tiles (elementwise, so the swizzled layout is irrelevant)
+    if constexpr (LT) {
+      // A row = X column quad * 32 + lane of the tile (box quad); K = 16 of the stage's 32 X rows.
+      // SW128_BASE32B: the 32-byte granule of a 128-byte row is XORed with (row & 3).
+      const int quad = warp & 3, half = lt_half(warp);
+      const uint32_t lane_off = uint32_t(quad * 32) << 16;
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t r0, r1;
+        unit_rows(u, r0, r1);
+        for (int64_t r = r0; r < r1; r += kBK, ++it) {
+          const int s = int(it % S);
+          if (lane == 0) tc::mbar_wait(&sm.full[s], (it / S) & 1);
+          __syncwarp();
+          const uint32_t box = tc::smem_u32(sm.x(s)) + uint32_t(quad) * 4096u + uint32_t(lane & 7) * 4u;
+          uint32_t v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int kr = half * 16 + i;
+            asm volatile("ld.shared.b32 %0, [%1];"
+                         : "=r"(v[i])
+                         : "r"(box + uint32_t(kr) * 128u + uint32_t(((lane >> 3) ^ (kr & 3)) << 5)) : "memory");
+          }
+          tc::tc_fence_after();
+#ifndef RNMF_TC_DBG_NOSPLIT
+          lt_store16(tmem_base + lane_off + uint32_t(C::kLoBase + s * kBK + half * 16), v);
+#endif
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&sm.lofull[s]);
+        }
+      }
+    } else if (X3) {  // 3xTF32 lo tiles (elementwise, so the swizzled layout is irrelevant)
       const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -456,8 +695,10 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
           const int s = int(it % S), j = int(it % kLoSlots);
           tc::mbar_wait(&sm.full[s], (it / S) & 1);
           tc::mbar_wait(&sm.loempty[j], ((it / kLoSlots) & 1) ^ 1);
+#ifndef RNMF_TC_DBG_NOSPLIT
           split_lo_tile<kXTileBytes / 16>(reinterpret_cast<const float4*>(sm.x(s)), reinterpret_cast<float4*>(sm.lo(j)), st);
           split_lo_tile<C::kSBytes / 16>(reinterpret_cast<const float4*>(sm.shi(s)), reinterpret_cast<float4*>(sm.slo(s)), st);
+#endif
           tc::fence_proxy_async_smem();
           tc::mbar_arrive(&sm.lofull[j]);
         }
@@ -480,7 +721,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1) tc_xtw_kernel(const __gri
         const int acc = C::kAccBufs == 2 ? int(ci & 1) : 0;
         tc::mbar_wait(&sm.tfull[acc], (C::kAccBufs == 2 ? ci >> 1 : ci) & 1);
         tc::tc_fence_after();
-        if (r0 < r1) drain_acc<NPAD, X3>(tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * C::kAccCols), a);
+        if (r0 < r1) drain_acc<NPAD, X3, !(LT && NPAD > 48)>(tmem_base + (uint32_t(sub * 32) << 16) + uint32_t(acc * C::kAccCols), a);
         tc::tc_fence_before();
         tc::mbar_arrive(&sm.tempty[acc]);
       }
@@ -566,37 +807,64 @@ int tc_chunk_stages() {
   return g_tc_chunk;
 }
 
+// LT (lo X tile in tensor memory) whenever its 448-thread CTA keeps the epilogue's NPAD fp32
+// accumulators in registers; RNMF_TC_NO_LT=1 forces the shared-memory lo ring (testing knob)
 template <int NPAD, bool X3>
-void tc_xw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
-                  int64_t ldst, int c, float* y, int sm_count, cudaStream_t stream) {
-  using C = TcCfg<NPAD, X3>;
+constexpr bool tc_lt_ok() { return X3 && NPAD <= 64; }
+inline bool tc_lt_enabled() {
+  static const bool off = std::getenv("RNMF_TC_NO_LT") != nullptr;
+  return !off;
+}
+
+template <int NPAD, bool X3, bool LT>
+void tc_xw_launch_lt(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
+                     int64_t ldst, int c, float* y, int sm_count, cudaStream_t stream) {
+  using C = TcCfg<NPAD, X3, LT>;
   const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBM);
   const CUtensorMap mh = make_map_2d(st_hi, NPAD, n, ldst, NPAD);
   const CUtensorMap ml = make_map_2d(st_lo, NPAD, n, ldst, NPAD);
   XwParams p{m, n, c, y, c, tc_chunk_stages()};
-  auto f = tc_xw_kernel<NPAD, X3>;
+  auto f = tc_xw_kernel<NPAD, X3, LT>;
   RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
   const int64_t ntiles = ceil_div(m, kBM);
   const int grid = int(std::min<int64_t>(ntiles, sm_count));
-  f<<<grid, tc_threads<X3>(), C::kSmem, stream>>>(mx, mh, ml, p);
+  f<<<grid, C::kThreads, C::kSmem, stream>>>(mx, mh, ml, p);
   RNMF_CUDA_LAUNCH();
 }
 
-
 template <int NPAD, bool X3>
-void tc_xtw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int64_t ldst,
-                   int c, float* part, int splits, int sm_count, cudaStream_t stream) {
-  using C = TcCfg<NPAD, X3>;
+void tc_xw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st_hi, const float* st_lo,
+                  int64_t ldst, int c, float* y, int sm_count, cudaStream_t stream) {
+  if constexpr (tc_lt_ok<NPAD, X3>()) {
+    if (tc_lt_enabled()) return tc_xw_launch_lt<NPAD, X3, true>(x, m, n, ldx, st_hi, st_lo, ldst, c, y, sm_count, stream);
+  }
+  tc_xw_launch_lt<NPAD, X3, false>(x, m, n, ldx, st_hi, st_lo, ldst, c, y, sm_count, stream);
+}
+
+template <int NPAD, bool X3, bool LT>
+void tc_xtw_launch_lt(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int64_t ldst,
+                      int c, float* part, int splits, int sm_count, cudaStream_t stream) {
+  using C = TcCfg<NPAD, X3, LT>;
   const CUtensorMap mx = make_map_2d(x, m, n, ldx, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);  // 32 x 32 boxes
   const CUtensorMap ms = make_map_2d(st, NPAD, m, ldst, NPAD);  // S^T: NPAD rows x m
   const CUtensorMap ml = make_map_2d(X3 ? st_lo : st, NPAD, m, ldst, NPAD);
   XtwParams p{m, n, c, splits, part, tc_chunk_stages()};
-  auto f = tc_xtw_kernel<NPAD, X3>;
+  auto f = tc_xtw_kernel<NPAD, X3, LT>;
   RNMF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem)));
   const int64_t units = ceil_div(n, 128) * splits;
   const int grid = int(std::min<int64_t>(units, sm_count));
-  f<<<grid, tc_threads<X3>(), C::kSmem, stream>>>(mx, ms, ml, p);
+  f<<<grid, C::kThreads, C::kSmem, stream>>>(mx, ms, ml, p);
   RNMF_CUDA_LAUNCH();
+}
+
+template <int NPAD, bool X3>
+void tc_xtw_launch(const float* x, int64_t m, int64_t n, int64_t ldx, const float* st, const float* st_lo, int64_t ldst,
+                   int c, float* part, int splits, int sm_count, cudaStream_t stream) {
+  if constexpr (tc_lt_ok<NPAD, X3>()) {
+    if (tc_lt_enabled())
+      return tc_xtw_launch_lt<NPAD, X3, true>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream);
+  }
+  tc_xtw_launch_lt<NPAD, X3, false>(x, m, n, ldx, st, st_lo, ldst, c, part, splits, sm_count, stream);
 }
 
 }  // namespace
@@ -659,6 +927,16 @@ int launch_tc_xtw(const float* x, int64_t m, int64_t n, int64_t ldx, const float
 
 namespace {
 }  // namespace
+
+#ifdef RNMF_TC_PROF
+void tc_prof_read(long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_tc_prof, sizeof(long long) * 16);
+  if (reset) {
+    long long z[16] = {};
+    cudaMemcpyToSymbol(g_tc_prof, z, sizeof z);
+  }
+}
+#endif
 
 int tc_npad(int c) { return int(ceil_div(c, 16) * 16); }
 
@@ -1490,37 +1768,49 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
       }
     }
   } else if (warp == 1) {
+    // UMMA issue: shared-memory descriptors as {lo, hi} words advanced by adds, ring indices kept
+    // incrementally (no make_sdesc / integer division per stage) -- the issuing thread's time per
+    // stage bounds this kernel (18 UMMAs and 3+ commits per 16 KB of X at k = 40)
     constexpr uint32_t idesc32 = tc::make_idesc_tf32(32, false, false);
     constexpr uint32_t idesc64 = tc::make_idesc_tf32(64, false, false);
-    auto adesc = [](uint32_t b, int k) { return tc::make_sdesc(b + k * 32, 16, 1024); };
-    uint32_t it = 0, ci = 0, ti = 0;
+    constexpr uint32_t idesc1 = tc::make_idesc_tf32(NPAD, false, false);
+    constexpr uint32_t idesc2 = tc::make_idesc_tf32(2 * NPAD, false, false);
+    constexpr uint32_t kHi = tc::sdesc_hi(1024, tc::kLayoutSW128);
+    const uint32_t x0 = (tc::smem_u32(xst(0)) >> 4) + tc::sdesc_lo_const(16);
+    const uint32_t l0 = (tc::smem_u32(lo(0)) >> 4) + tc::sdesc_lo_const(16);
+    uint32_t ci = 0, ti = 0;
+    uint32_t s = 0, sph = 0, j = 0, jph = 0, b = 0, bph = 0;
     uint32_t d = tmem_base;
     const uint32_t wa_hi = tmem_base + uint32_t(C::kWBase), wa_lo = wa_hi + 64u;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ti) {
       tc::mbar_wait(wfull, ti & 1);  // this tile's W rows are in TMEM
       tc::tc_fence_after();
-      for (int kc = 0; kc < nk; ++kc, ++it) {
-        const int kin = kc % p.chunk;
+      int kin = 0;
+      for (int kc = 0; kc < nk; ++kc) {
         const bool cend = (kin == p.chunk - 1) || (kc == nk - 1);
         const int acc = int(ci & 1);
         if (kin == 0) {
           tc::mbar_wait(&tempty[acc], ((ci >> 1) & 1) ^ 1);
           d = tmem_base + uint32_t(acc * C::kAccCols);
         }
-        const int s = int(it % S), j = int(it % LO), b = int(it % RB);
-        tc::mbar_wait(&rempty[b], ((it / RB) & 1) ^ 1);
-        tc::mbar_wait(&full[s], (it / S) & 1);
-        tc::mbar_wait(&lofull[j], (it / LO) & 1);
+        tc::mbar_wait(&rempty[b], bph ^ 1);
+        tc::mbar_wait(&full[s], sph);
+        tc::mbar_wait(&lofull[j], jph);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          issue_stage<NPAD, true, false>(d, tc::smem_u32(xst(s)), tc::smem_u32(lo(j)), tc::smem_u32(shi(s)), kin == 0,
-                                         adesc);
-          const uint32_t dr = tmem_base + uint32_t(C::kRsBase + b * 64);
-          const uint32_t ha = tc::smem_u32(htp(s));
+          const uint32_t xa = x0 + s * uint32_t(C::kStageBytes >> 4), ba = xa + uint32_t(kXTileBytes >> 4);
+          const uint32_t la = l0 + j * uint32_t(kXTileBytes >> 4);
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            tc::umma_tf32_w(d, xa + 2 * k, kHi, ba + 2 * k, kHi, idesc2, (kin == 0 && k == 0) ? 0u : 1u);  // X_hi [S_hi; S_lo]
+            tc::umma_tf32_w(d + NPAD, la + 2 * k, kHi, ba + 2 * k, kHi, idesc1, 1u);                       // += X_lo S_hi
+          }
+          const uint32_t dr = tmem_base + uint32_t(C::kRsBase) + b * 64u;
+          const uint32_t ha = ba + uint32_t((2 * C::kSBytes) >> 4);  // H^T slab: two 32-wide K atoms of (hi | lo) rows
           for (int kk = 0; kk < ks; ++kk) {
-            const uint64_t hb = tc::make_sdesc(ha + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-            tc::umma_tf32_ts(dr, wa_hi + uint32_t(kk * 8), hb, idesc64, kk != 0);  // [W_hi H_hi | W_hi H_lo]
-            tc::umma_tf32_ts(dr + 32, wa_lo + uint32_t(kk * 8), hb, idesc32, 1u);  // += W_lo H_hi
+            const uint32_t hb = ha + uint32_t((kk >> 2) * (8192 >> 4) + (kk & 3) * 2);
+            tc::umma_tf32_ts_w(dr, wa_hi + uint32_t(kk * 8), hb, kHi, idesc64, kk != 0);  // [W_hi H_hi | W_hi H_lo]
+            tc::umma_tf32_ts_w(dr + 32, wa_lo + uint32_t(kk * 8), hb, kHi, idesc32, 1u);  // += W_lo H_hi
           }
           tc::umma_commit(&empty[s]);
           tc::umma_commit(&loempty[j]);
@@ -1528,8 +1818,16 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
           if (cend) tc::umma_commit(&tfull[acc]);
           if (kc == nk - 1) tc::umma_commit(wempty);
         }
-        if (cend) ++ci;
         __syncwarp();
+        if (cend) {
+          ++ci;
+          kin = 0;
+        } else {
+          ++kin;
+        }
+        if (++s == uint32_t(S)) s = 0, sph ^= 1;
+        if (++j == uint32_t(LO)) j = 0, jph ^= 1;
+        if (++b == uint32_t(RB)) b = 0, bph ^= 1;
       }
     }
   } else if (warp < 4 || warp >= 8) {

@@ -14,6 +14,9 @@
 #include "kernels.h"
 
 using namespace rnmf_gpu;
+#ifdef RNMF_TC_PROF
+namespace rnmf_gpu { void tc_prof_read(long long* out, bool reset); }
+#endif
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { std::printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); std::exit(1); } } while (0)
 
@@ -134,7 +137,20 @@ int main(int argc, char** argv) {
       for (int ch : {16, 8, 4}) {
         if (!x3 && ch != 2) continue;
         tc_set_chunk(ch);
+#ifdef RNMF_TC_PROF
+        { long long z[16]; tc_prof_read(z, true); }
+#endif
         ms = timeit([&] { launch_tc_xw(dx, m, n, ldx, dh, dl, c, dy, x3, sms, 0); });
+#ifdef RNMF_TC_PROF
+        {
+          long long z[16];
+          tc_prof_read(z, true);
+          const double stages = double((m + 127) / 128 + sms - 1) / sms * double((n + 31) / 32) * (reps + 1);
+          const char* nm2[] = {"producer wait empty", "mma wait tempty", "mma wait full", "mma wait lofull", "mma issue",
+                               "split wait full", "split work", "epi wait tfull", "epi drain"};
+          for (int i = 0; i < 9; ++i) std::printf("   prof %-20s %9.1f cycles / stage\n", nm2[i], double(z[i]) / stages);
+        }
+#endif
         char nm[64];
         std::snprintf(nm, sizeof nm, "tc%s chunk=%d", x3 ? "3xtf32" : "1xtf32", ch);
         report(nm, ms);
