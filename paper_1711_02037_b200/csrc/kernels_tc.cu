@@ -60,21 +60,23 @@ __device__ __forceinline__ float tf32_lo(float v) {
 }
 
 __device__ __forceinline__ uint32_t tf32_lo_bits(uint32_t u) {
-  // d = x - trunc_tf32(x) (exact), then round d to tf32, nearest with ties away (= cvt.rna.tf32)
+  // d = x - trunc_tf32(x) (exact), then round d to tf32, nearest with ties away (= cvt.rna.tf32).
+  // The low 13 bits are left as they fall: the only reader is kind::tf32, which ignores them (one
+  // ALU op less per element; under the 1000 W cap these kernels are power-bound).
   const uint32_t d = __float_as_uint(__uint_as_float(u) - __uint_as_float(u & 0xffffe000u));
-  return (d + 0x1000u) & 0xffffe000u;
+  return d + 0x1000u;
 }
 
 // lo part of one X stage (N16 float4s) by kSplitThreads threads: explicit shared-space vector
 // loads / stores (the tile pointers are generic in C++), all loads of a thread issued first
-template <int N16>
+template <int N16, int NT = kSplitThreads>
 __device__ __forceinline__ void split_lo_tile(const float4* __restrict__ x4, float4* __restrict__ l4, int st) {
-  constexpr int kIt = (N16 + kSplitThreads - 1) / kSplitThreads;
+  constexpr int kIt = (N16 + NT - 1) / NT;
   const uint32_t xs = tc::smem_u32(x4), ls = tc::smem_u32(l4);
   uint32_t v[kIt][4];
 #pragma unroll
   for (int i = 0; i < kIt; ++i) {
-    const int q = st + i * kSplitThreads;
+    const int q = st + i * NT;
     if (q < N16)
       asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                    : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3])
@@ -82,7 +84,7 @@ __device__ __forceinline__ void split_lo_tile(const float4* __restrict__ x4, flo
   }
 #pragma unroll
   for (int i = 0; i < kIt; ++i) {
-    const int q = st + i * kSplitThreads;
+    const int q = st + i * NT;
     if (q < N16)
       asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ls + 16u * uint32_t(q)), "r"(tf32_lo_bits(v[i][0])),
                    "r"(tf32_lo_bits(v[i][1])), "r"(tf32_lo_bits(v[i][2])), "r"(tf32_lo_bits(v[i][3]))
@@ -544,11 +546,13 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_ker
           const int s = int(it % S);
           tc::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
           // 3xTF32: the raw S^T slab only; its lo slab is written on chip by the split warps
-          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes + C::kSBytes * (LT ? 2 : 1)));
+          // the S^T slab raw only: its lo slab is written on chip by the split warps (S^T = Q^T is
+          // l x m here, re-read by every column tile; loading a second copy through L2 cost 7 % more
+          // DRAM traffic than splitting on chip)
+          tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes + C::kSBytes));
 #pragma unroll
           for (int b = 0; b < 4; ++b) tc::tma_load_2d(sm.x(s) + b * 4096, &tmX, &sm.full[s], int(ct * 128 + b * 32), int(r));
           tc::tma_load_2d(sm.shi(s), &tmSt, &sm.full[s], int(r), 0);
-          if (LT) tc::tma_load_2d(sm.slo(s), &tmStLo, &sm.full[s], int(r), 0);
         }
       }
     }
@@ -680,6 +684,9 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_ker
           tc::tc_fence_after();
 #ifndef RNMF_TC_DBG_NOSPLIT
           lt_store16(tmem_base + lane_off + uint32_t(C::kLoBase + s * kBK + half * 16), v);
+          split_lo_tile<C::kSBytes / 16, 256>(reinterpret_cast<const float4*>(sm.shi(s)),
+                                              reinterpret_cast<float4*>(sm.slo(s)), (quad * 2 + half) * 32 + lane);
+          tc::fence_proxy_async_smem();
 #endif
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&sm.lofull[s]);

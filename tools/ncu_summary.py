@@ -83,7 +83,7 @@ def main(src, dst, cfg):
                     f"{cfg} --steps 1 --warmup 3 (cold-cache, serialised: compare shares)\n")
             f.write(launch_summary(lp))
     kernels = {}
-    for name in ("rhals_sweeps_kernel", "tc_xht_resid_kernel", "tc_resid_kernel", "metrics_kernel", "tc_xw_kernel", "tc_xtw_kernel", "xw_tma_kernel", "xtw_tma_kernel"):
+    for name in ("rhals_sweeps_kernel", "tc_xht_resid_w_kernel", "tc_xht_resid_kernel", "tc_resid_kernel", "metrics_kernel", "tc_xw_kernel", "tc_xtw_kernel", "xw_tma_kernel", "xtw_tma_kernel"):
         rep = os.path.join(src, f"{name}_{cfg}.ncu-rep")
         if os.path.exists(rep):
             kernels[name] = kernel_metrics(rep)

@@ -14,13 +14,13 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
   python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
 echo "launch list rc=$?"
 timeout 300 python tools/run_fit.py --config $CFG --fits 1 > $OUT/fit.json 2>&1 || { echo "fit failed"; exit 1; }
-for K in rhals_sweeps_kernel tc_xht_resid_kernel tc_xw_kernel tc_xtw_kernel; do
+for K in rhals_sweeps_kernel tc_xht_resid_w_kernel tc_xw_kernel tc_xtw_kernel; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -s 1 -c 1 \
     -o $OUT/${K}_${CFG} python tools/run_fit.py --config $CFG --fits 1 > $OUT/ncu_${K}.log 2>&1
   echo "ncu $K rc=$?"
 done
 # other configs (bench lines) and the accuracy / streaming probes
-for C2 in C3 C4 C1; do
+for C2 in C2 C3 C1 C5; do
   timeout 600 python bench.py --config $C2 --steps 3 --no-cpu-baseline > $OUT/bench_$C2.json 2> $OUT/bench_$C2.err
   echo "bench $C2 rc=$?"
 done
