@@ -224,6 +224,21 @@ int64_t cholqr_workspace_doubles(int64_t rows, int l) {
   return int64_t(gram_blocks(rows)) * l * l + 2 * int64_t(l) * l + rows * int64_t(l) + 64;
 }
 
+// Dynamic shared-memory limit of a kernel, raised (never lowered) when a launch needs more than any
+// launch before it on this device: one table keyed by the kernel, shared by every instantiation
+// of launch_cholqr2 (cq_chol_kernel and the double kernels serve both precisions).
+static std::mutex g_cq_attr_mu;
+static std::map<std::pair<int, const void*>, size_t> g_cq_attr;
+
+template <typename F>
+static void cq_raise_smem(int dev, F* kernel, size_t bytes) {
+  size_t& have = g_cq_attr[{dev, reinterpret_cast<const void*>(kernel)}];
+  if (bytes > have) {
+    RNMF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    have = bytes;
+  }
+}
+
 template <typename T>
 int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* flag, cudaStream_t stream,
                    const GramAllreduce* allreduce, double shift_rel) {
@@ -237,30 +252,17 @@ int launch_cholqr2(const T* a, int64_t rows, int l, T* q_out, double* ws, int* f
   const size_t csm = size_t(2) * l * (l + 1) * sizeof(double);
   const size_t asm_ = size_t(l) * (l + 1) * sizeof(double) + size_t(64) * (l + 1) * sizeof(double);
   RNMF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream));
-  // dynamic shared-memory attributes (chol needs 2 l (l+1) doubles: l <= 112 on B200), raised per
-  // device only when a larger l than before arrives (the sizes grow with l); cq_chol_kernel and the
-  // double instantiations are shared by both precisions, so one table covers every kernel
+  // dynamic shared-memory limits (chol needs 2 l (l+1) doubles: l <= 112 on B200)
   {
-    static std::mutex mu;
-    static std::map<std::pair<int, int>, int> done_l;  // (device, sizeof(T)) -> largest l configured
     int dev = 0;
     RNMF_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(mu);
-    int& have_t = done_l[{dev, int(sizeof(T))}];
-    int& have_d = done_l[{dev, 0}];  // kernels shared by both precisions
-    if (l > have_t) {
-      RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
-      RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_)));
-      RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
-      have_t = l;
-    }
-    if (l > have_d) {
-      RNMF_CUDA(cudaFuncSetAttribute(cq_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)));
-      RNMF_CUDA(cudaFuncSetAttribute(cq_apply_kernel<double, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(asm_)));
-      RNMF_CUDA(cudaFuncSetAttribute(cq_gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm)));
-      have_d = l;
-    }
+    std::lock_guard<std::mutex> lock(g_cq_attr_mu);
+    cq_raise_smem(dev, cq_apply_kernel<T, double>, asm_);
+    cq_raise_smem(dev, cq_apply_kernel<double, T>, asm_);
+    cq_raise_smem(dev, cq_apply_kernel<double, double>, asm_);
+    cq_raise_smem(dev, cq_gram_kernel<T>, gsm);
+    cq_raise_smem(dev, cq_gram_kernel<double>, gsm);
+    cq_raise_smem(dev, cq_chol_kernel, csm);
   }
   const int ab = int(std::max<int64_t>(1, std::min<int64_t>(148 * 4, ceil_div(rows, 64))));
   int launches = 0;

@@ -651,11 +651,8 @@ struct Sweeper {
     if constexpr (F32S) {
       for (int i = tid; i < LREG; i += kSwThreads) cnf[i] = 0.f;
       // W rows of this CTA into the column-major scratch (the launch works column by column)
-      for (int64_t e = tid; e < R * k; e += kSwThreads) {
-        const int64_t r = e / k;
-        const int j = int(e % k);
-        a.wc[int64_t(j) * a.m + r0 + r] = float(a.w[(r0 + r) * k + j]);
-      }
+      for (int j = 0; j < k; ++j)
+        for (int64_t r = tid; r < R; r += kSwThreads) a.wc[int64_t(j) * a.m + r0 + r] = float(a.w[(r0 + r) * k + j]);
     }
     if constexpr (QS) {
       for (int64_t e = tid; e < R * l; e += kSwThreads) {
@@ -699,11 +696,8 @@ struct Sweeper {
   __device__ void store_back(int64_t last, int stopped) {
     if constexpr (F32S) {
       if ((a.flags & kDoW) || a.order != nullptr)
-        for (int64_t e = tid; e < R * k; e += kSwThreads) {
-          const int64_t r = e / k;
-          const int j = int(e % k);
-          a.w[(r0 + r) * k + j] = T(a.wc[int64_t(j) * a.m + r0 + r]);
-        }
+        for (int j = 0; j < k; ++j)
+          for (int64_t r = tid; r < R; r += kSwThreads) a.w[(r0 + r) * k + j] = T(a.wc[int64_t(j) * a.m + r0 + r]);
     }
     if constexpr (QS) {
       for (int64_t e = tid; e < R * k; e += kSwThreads) {
@@ -1751,19 +1745,33 @@ struct Sweeper {
         ef[e] = j < k ? float(Ep[i * es + j]) : 0.f;
       }
       __syncthreads();
+      // UNR rows per thread: all their Q / W loads are in flight together (the pass streams the Q
+      // slab and W from L2) and every broadcast load of E feeds UNR rows' FMAs
       constexpr int L4 = LREG / 4;
+      constexpr int UNR = LREG <= 32 ? 4 : 2;
       const float4* q4 = reinterpret_cast<const float4*>(a.q4);
-      for (int64_t r = tid; r < R; r += kSwThreads) {
-        float4 qv[L4];
+      for (int64_t rb = tid; rb < R; rb += int64_t(kSwThreads) * UNR) {
+        float4 qv[UNR][L4];
+        int64_t rr[UNR];
 #pragma unroll
-        for (int i4 = 0; i4 < L4; ++i4) qv[i4] = __ldg(q4 + int64_t(i4) * a.m + r0 + r);
-        float accf = 0.f;
+        for (int uu = 0; uu < UNR; ++uu) {
+          const int64_t r = rb + int64_t(kSwThreads) * uu;
+          rr[uu] = r < R ? r0 + r : r0;  // clamped: in-range address, result unused
+#pragma unroll
+          for (int i4 = 0; i4 < L4; ++i4) qv[uu][i4] = __ldg(q4 + int64_t(i4) * a.m + rr[uu]);
+        }
+        float accf[UNR];
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu) accf[uu] = 0.f;
         for (int j0 = 0; j0 < k; j0 += 8) {
-          float sacc[8], wv[8];
+          float sacc[UNR][8], wv[UNR][8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            sacc[t] = 0.f;
-            wv[t] = j0 + t < k ? a.wc[int64_t(j0 + t) * a.m + r0 + r] : 0.f;
+          for (int uu = 0; uu < UNR; ++uu) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              sacc[uu][t] = 0.f;
+              wv[uu][t] = j0 + t < k ? a.wc[int64_t(j0 + t) * a.m + rr[uu]] : 0.f;
+            }
           }
 #pragma unroll
           for (int i4 = 0; i4 < L4; ++i4) {
@@ -1771,30 +1779,38 @@ struct Sweeper {
             for (int c = 0; c < 4; ++c) {
               const int i = 4 * i4 + c;
               if (i < l) {
-                const float qv1 = c == 0 ? qv[i4].x : c == 1 ? qv[i4].y : c == 2 ? qv[i4].z : qv[i4].w;
                 const float4* ei = reinterpret_cast<const float4*>(ef + i * k8 + j0);
                 const float4 e0 = ei[0], e1 = ei[1];
-                sacc[0] = fmaf(qv1, e0.x, sacc[0]);
-                sacc[1] = fmaf(qv1, e0.y, sacc[1]);
-                sacc[2] = fmaf(qv1, e0.z, sacc[2]);
-                sacc[3] = fmaf(qv1, e0.w, sacc[3]);
-                sacc[4] = fmaf(qv1, e1.x, sacc[4]);
-                sacc[5] = fmaf(qv1, e1.y, sacc[5]);
-                sacc[6] = fmaf(qv1, e1.z, sacc[6]);
-                sacc[7] = fmaf(qv1, e1.w, sacc[7]);
+#pragma unroll
+                for (int uu = 0; uu < UNR; ++uu) {
+                  const float qv1 = c == 0 ? qv[uu][i4].x : c == 1 ? qv[uu][i4].y : c == 2 ? qv[uu][i4].z : qv[uu][i4].w;
+                  sacc[uu][0] = fmaf(qv1, e0.x, sacc[uu][0]);
+                  sacc[uu][1] = fmaf(qv1, e0.y, sacc[uu][1]);
+                  sacc[uu][2] = fmaf(qv1, e0.z, sacc[uu][2]);
+                  sacc[uu][3] = fmaf(qv1, e0.w, sacc[uu][3]);
+                  sacc[uu][4] = fmaf(qv1, e1.x, sacc[uu][4]);
+                  sacc[uu][5] = fmaf(qv1, e1.y, sacc[uu][5]);
+                  sacc[uu][6] = fmaf(qv1, e1.z, sacc[uu][6]);
+                  sacc[uu][7] = fmaf(qv1, e1.w, sacc[uu][7]);
+                }
               }
             }
           }
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            if (j0 + t < k) {
-              const float gv = -2.f * sacc[t];
-              const float gp = wv[t] > 0.f ? gv : fminf(0.f, gv);
-              accf = fmaf(gp, gp, accf);
+          for (int uu = 0; uu < UNR; ++uu) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (j0 + t < k) {
+                const float gv = -2.f * sacc[uu][t];
+                const float gp = wv[uu][t] > 0.f ? gv : fminf(0.f, gv);
+                accf[uu] = fmaf(gp, gp, accf[uu]);
+              }
             }
           }
         }
-        acc += double(accf);
+#pragma unroll
+        for (int uu = 0; uu < UNR; ++uu)
+          if (rb + int64_t(kSwThreads) * uu < R) acc += double(accf[uu]);
       }
     } else if constexpr (!QS && LREG > 0) {
       constexpr int UNR = (sizeof(T) == 4 && LREG <= 32) ? 4 : 1;

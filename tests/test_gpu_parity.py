@@ -279,3 +279,19 @@ def test_sweep_kernel_paths(gpu, oracle, knobs, dtype, monkeypatch):
     res = gpu.rhals_fit(x.astype(dtype), o, omega=om, w0=w0, h0=h0)
     rtol = F64_TRACE_RTOL if dtype == np.float64 else F32_TRACE_RTOL
     assert_trace_close(res.trace, ref.trace, rtol, F32_FINAL_ATOL)
+
+
+def test_qr_limits_across_precisions_and_widths(gpu, oracle):
+    """Fits of different precisions and sketch widths in one process, widest fp32 first: the
+    CholeskyQR kernels' dynamic shared-memory limits are configured once per (device, largest l) and
+    shared by both precisions (a per-precision table once let an fp64 fit with a narrow sketch lower
+    the limit an earlier wide fp32 fit had set, and the next fp32 fit failed to launch)."""
+    for dtype, m, n, k, p in ((np.float32, 700, 500, 40, 20), (np.float64, 300, 200, 4, 3),
+                              (np.float32, 600, 400, 16, 20), (np.float64, 400, 300, 30, 20),
+                              (np.float32, 500, 300, 8, 4)):
+        x = oracle.synth_lowrank(m, n, k, 0.05, 5 + m).astype(dtype)
+        o = _opts(gpu, rank=k, max_iter=5, tol=1e-300, oversampling=p, power_iterations=1, seed=3)
+        res = gpu.rhals_fit(x, o)
+        ref = oracle.rhals_fit(x.astype(np.float64), _odict(o))
+        rtol = F64_TRACE_RTOL if dtype == np.float64 else F32_TRACE_RTOL
+        assert_trace_close(res.trace, ref.trace, rtol, fields=("rel_err",))
