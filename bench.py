@@ -168,7 +168,10 @@ def make_workload(cfg_name: str, device, world: int = 1, rank: int = 0, sharded:
 # 10 sweeps (10 sweeps = one full-space metrics period), and the full fit is extrapolated with
 # t(m, s) = A(m) + (s / 10) P(m), A and P linear in m (sketch / metrics / W-phase work is linear
 # in m at fixed n; the H phase is independent of m).  Labelled "extrapolated".
-SLICE_ROWS = {"C4": (1000, 3000), "C5": (250, 750)}
+# slice heights: tall enough that the m-dependent part of a 10-sweep period (W phase, metrics)
+# stands out of the m-independent H phase and of host timing jitter (1,000 / 3,000-row slices gave
+# 85 - 550 s for the same C4 fit), short enough for ~15 - 25 s of CPU work in total
+SLICE_ROWS = {"C4": (2000, 10000), "C5": (500, 2500)}
 
 
 def _oracle_fit_s(orc, x64, cfg, omega, w0, h0, sweeps):

@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(kThreads) xtw_metrics_reduce_kernel(const T* _
                                                                       const double* __restrict__ wtw,
                                                                       double* part_pgh) {
   __shared__ double gsum[kGhGroups][kGhEntries];
+  __shared__ double bsum[kGhGroups][kGhEntries];
   __shared__ double red[kThreads / 32];
   const int ei = threadIdx.x % kGhEntries, gi = threadIdx.x / kGhEntries;
   const int64_t e = int64_t(blockIdx.x) * kGhEntries + ei;  // e = col * k + j
@@ -444,16 +445,21 @@ __global__ void __launch_bounds__(kThreads) xtw_metrics_reduce_kernel(const T* _
     for (; s < splits; s += kGhGroups) a[0] += double(part[int64_t(s) * total + e]);
   }
   gsum[gi][ei] = (a[0] + a[1]) + (a[2] + a[3]);
+  // ((W^T W) H)(j, col): the k-long dot product split over the 4 groups as well (t = gi, gi + 4, ..)
+  const int64_t col = e < total ? e / k : 0;
+  const int j = e < total ? int(e - col * k) : 0;
+  double bp = 0.0;
+  if (e < total)
+    for (int t = gi; t < k; t += kGhGroups) bp += wtw[j * k + t] * double(H[int64_t(t) * n + col]);
+  bsum[gi][ei] = bp;
   __syncthreads();
   double acc = 0.0;
   if (gi == 0 && e < total) {
-    double wx = 0.0;
+    double wx = 0.0, b = 0.0;
 #pragma unroll
     for (int g = 0; g < kGhGroups; ++g) wx += gsum[g][ei];
-    const int64_t col = e / k;
-    const int j = int(e % k);
-    double b = 0.0;
-    for (int t = 0; t < k; ++t) b += wtw[j * k + t] * double(H[int64_t(t) * n + col]);
+#pragma unroll
+    for (int g = 0; g < kGhGroups; ++g) b += bsum[g][ei];
     const double g = -2.0 * (wx - b);
     const double hv = double(H[int64_t(j) * n + col]);
     const double gp = hv > 0.0 ? g : fmin(g, 0.0);
@@ -474,34 +480,62 @@ constexpr int kGramChunk = 64;
 constexpr int kGramAcc = 16;  // entries per thread -> c <= 64
 
 // part[b] = A[rows of b]^T A[rows of b] (c x c), rows split evenly over gridDim.x CTAs.
+// Register-blocked: thread (block bi, bj; row group grp) keeps a 4 x 4 block of the Gram in fp64
+// registers and walks the rows grp, grp + G, .. of each 64-row chunk (two 16-byte loads per operand
+// for 16 DFMAs; the one-entry-per-thread version was shared-memory-load bound, 170 us at C4 size);
+// the G row groups are summed in a fixed order at the end.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) gram_rows_kernel(const T* __restrict__ A, int64_t rows, int c,
                                                              double* part) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* tile = reinterpret_cast<double*>(smem);  // [kGramChunk][c]
+  double* tile = reinterpret_cast<double*>(smem);  // [kGramChunk][cp], reused as red[G][cp * cp]
+  const int cp = (c + 3) & ~3;
+  const int nb = cp / 4, nblk = nb * nb;
+  const int G = kThreads / nblk;  // >= 1 for c <= 64
+  const int tid = threadIdx.x;
+  const int blk = tid % nblk, grp = tid / nblk;
+  const bool active = grp < G;
+  const int bi = blk / nb, bj = blk % nb;
   const int64_t r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
   const int cc = c * c;
-  double acc[kGramAcc] = {};  // entries tid + 256 u
+  double acc[4][4] = {};
+  for (int e = tid; e < kGramChunk * cp; e += kThreads) tile[e] = 0.0;  // the pad columns stay zero
   for (int64_t base = r0; base < r1; base += kGramChunk) {
     const int nr = int(r1 - base < kGramChunk ? r1 - base : kGramChunk);
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * c; e += kThreads) tile[e] = double(A[(base + e / c) * c + e % c]);
+    const T* src = A + base * c;  // nr rows, contiguous
+    for (int e = tid; e < nr * c; e += kThreads) {
+      const int r = e / c;
+      tile[r * cp + (e - r * c)] = double(src[e]);
+    }
     __syncthreads();
+    if (active) {
+      for (int r = grp; r < nr; r += G) {
+        const double2* ta = reinterpret_cast<const double2*>(tile + r * cp + 4 * bi);
+        const double2* tb = reinterpret_cast<const double2*>(tile + r * cp + 4 * bj);
+        const double2 a0 = ta[0], a1 = ta[1], b0 = tb[0], b1 = tb[1];
+        const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-    for (int u = 0; u < kGramAcc; ++u) {
-      const int e = threadIdx.x + kThreads * u;
-      if (e < cc) {
-        const int a = e / c, b = e % c;
-        double s = acc[u];
-        for (int r = 0; r < nr; ++r) s += tile[r * c + a] * tile[r * c + b];
-        acc[u] = s;
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] += av[x] * bv[y];
       }
     }
   }
+  __syncthreads();
+  double* red = tile;
+  if (active) {
 #pragma unroll
-  for (int u = 0; u < kGramAcc; ++u) {
-    const int e = threadIdx.x + kThreads * u;
-    if (e < cc) part[int64_t(blockIdx.x) * cc + e] = acc[u];
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) red[grp * cp * cp + (4 * bi + x) * cp + 4 * bj + y] = acc[x][y];
+  }
+  __syncthreads();
+  for (int e = tid; e < cc; e += kThreads) {
+    const int i = e / c, j = e - i * c;
+    double sum = 0.0;
+    for (int g2 = 0; g2 < G; ++g2) sum += red[g2 * cp * cp + i * cp + j];
+    part[int64_t(blockIdx.x) * cc + e] = sum;
   }
 }
 
@@ -779,7 +813,8 @@ template <typename T>
 int launch_gram_rows(const T* a, int64_t rows, int c, double* part, double* g, cudaStream_t stream) {
   if (c > 64) throw CudaError("gram: column count above 64 not supported");
   const int np = gram_parts(rows);
-  const size_t sm = size_t(kGramChunk) * c * sizeof(double);
+  const int cp = (c + 3) & ~3, groups = kThreads / ((cp / 4) * (cp / 4));
+  const size_t sm = size_t(std::max(kGramChunk * cp, groups * cp * cp)) * sizeof(double);
   gram_rows_kernel<T><<<np, kThreads, sm, stream>>>(a, rows, c, part);
   RNMF_CUDA_LAUNCH();
   reduce_parts_kernel<<<unsigned(ceil_div(c * c, 32)), 256, 0, stream>>>(part, np, c * c, g);
