@@ -51,6 +51,12 @@ constexpr int kXTileBytes = kBM * kBK * 4;  // 16 KB: one X stage (either kernel
 #endif
 constexpr int kLoSlots = RNMF_TC_LO_SLOTS;  // 3xTF32 lo-tile ring
 constexpr int kSmemBudget = RNMF_TC_SMEM_KB * 1024;
+// L2 eviction priorities of the TMA loads (RNMF_TC_NO_L2_HINT: both normal, for comparison)
+#ifdef RNMF_TC_NO_L2_HINT
+constexpr uint64_t kXPolicy = 0x1000000000000000ull, kSPolicy = 0x1000000000000000ull;
+#else
+constexpr uint64_t kXPolicy = tc::kL2EvictFirst, kSPolicy = tc::kL2EvictLast;
+#endif
 
 // 3xTF32 operand split.  hi = the raw fp32 word: kind::tf32 reads only the top 19 bits, i.e. it
 // truncates, so lo = rna_tf32(x - trunc_tf32(x)) is what the tensor core misses.  Only lo is
@@ -308,14 +314,14 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xw_kern
 #ifdef RNMF_TC_DBG_NOSLOAD  // (experiment) the S slab only on the first pass over the ring
           if (it >= uint32_t(S)) {
             tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes));
-            tc::tma_load_2d(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM));
+            tc::tma_load_2d_hint(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM), kXPolicy);
             continue;
           }
 #endif
           tc::mbar_arrive_expect_tx(&sm.full[s], bytes);
-          tc::tma_load_2d(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM));
-          tc::tma_load_2d(sm.shi(s), &tmShi, &sm.full[s], kc * kBK, 0);
-          if (LT) tc::tma_load_2d(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0);
+          tc::tma_load_2d_hint(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM), kXPolicy);
+          tc::tma_load_2d_hint(sm.shi(s), &tmShi, &sm.full[s], kc * kBK, 0, kSPolicy);
+          if (LT) tc::tma_load_2d_hint(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0, kSPolicy);
         }
       }
     }
@@ -551,8 +557,9 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_ker
           // DRAM traffic than splitting on chip)
           tc::mbar_arrive_expect_tx(&sm.full[s], uint32_t(kXTileBytes + C::kSBytes));
 #pragma unroll
-          for (int b = 0; b < 4; ++b) tc::tma_load_2d(sm.x(s) + b * 4096, &tmX, &sm.full[s], int(ct * 128 + b * 32), int(r));
-          tc::tma_load_2d(sm.shi(s), &tmSt, &sm.full[s], int(r), 0);
+          for (int b = 0; b < 4; ++b)
+            tc::tma_load_2d_hint(sm.x(s) + b * 4096, &tmX, &sm.full[s], int(ct * 128 + b * 32), int(r), kXPolicy);
+          tc::tma_load_2d_hint(sm.shi(s), &tmSt, &sm.full[s], int(r), 0, kSPolicy);
         }
       }
     }
@@ -1082,7 +1089,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) tc_resid_kernel(const __grid_co
           const int s = int(it % S);
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
-          tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
+          tc::tma_load_2d_hint(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM), kXPolicy);
 #pragma unroll
           for (int a = 0; a < C::kAtoms; ++a) {
             tc::tma_load_2d(hst(s) + a * C::kHtAtomBytes, &tmHhi, &full[s], a * 32, kc * kBK);
@@ -1502,7 +1509,7 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_kernel(
           // X and the H / H^T slabs with their lo parts (prepared once per evaluation): the split
           // warps, the busiest role of this kernel, only split X
           tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
-          tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
+          tc::tma_load_2d_hint(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM), kXPolicy);
           tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
           tc::tma_load_2d(shi(s) + C::kSBytes, &tmSlo, &full[s], kc * kBK, 0);
           tc::tma_load_2d(htp(s), &tmHhi, &full[s], 0, kc * kBK);
@@ -1763,7 +1770,7 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           // X and the H / H^T slabs with their lo parts: the split warps only split X
           tc::mbar_arrive_expect_tx(&full[s], uint32_t(C::kStageBytes));
-          tc::tma_load_2d(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM));
+          tc::tma_load_2d_hint(xst(s), &tmX, &full[s], kc * kBK, int(t * kBM), kXPolicy);
           tc::tma_load_2d(shi(s), &tmShi, &full[s], kc * kBK, 0);
           tc::tma_load_2d(shi(s) + C::kSBytes, &tmSlo, &full[s], kc * kBK, 0);
 #pragma unroll
