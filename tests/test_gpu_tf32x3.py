@@ -91,3 +91,22 @@ def test_tf32x3_edge_shapes(gpu, oracle, m, n, k):
     res = gpu.rhals_fit(x.astype(np.float32), o, omega=om, w0=w0, h0=h0)
     assert len(res.trace) == len(ref.trace)
     assert abs(res.trace[-1].rel_err - ref.trace[-1]["rel_err"]) <= 1e-4 + 1e-3 * ref.trace[-1]["rel_err"]
+
+
+@pytest.mark.parametrize("m,n,k,p", [(20000, 3000, 40, 20), (30011, 777, 16, 20), (9000, 5000, 10, 6)])
+def test_tf32x3_bitwise_repeatable(gpu, m, n, k, p):
+    """Three fits of the same inputs give identical bits (W, H and every trace field).  The
+    tensor-core kernels hand tiles between the TMA, split, UMMA and epilogue warps through
+    mbarriers and tensor memory; a missed wait or a slot reused too early would show up here as
+    run-to-run differences.  Shapes: many persistent tiles per CTA, ragged tails, l = 60 / 36 / 16."""
+    x = workloads.noisy_lowrank_matrix(3, m, n, k, 0.5, 0.1)
+    o = gpu.SolverOptions(rank=k, max_iter=12, tol=1e-300, oversampling=p, power_iterations=2, seed=5,
+                          trace_full_every=3)
+    o.math_mode = gpu.MathMode.TF32x3
+    runs = [gpu.rhals_fit(x, o) for _ in range(3)]
+    for r in runs[1:]:
+        np.testing.assert_array_equal(runs[0].factors.w, r.factors.w)
+        np.testing.assert_array_equal(runs[0].factors.h, r.factors.h)
+        for a, b in zip(runs[0].trace, r.trace):
+            assert (a.objective, a.rel_err, a.pgrad, a.pgrad_full, a.objective_compressed) == \
+                   (b.objective, b.rel_err, b.pgrad, b.pgrad_full, b.objective_compressed)
