@@ -1481,8 +1481,14 @@ struct Sweeper {
       if constexpr (kHCap >= 32) {
         if (kh == 32)
           h_cols_lane<32>(update, grad_valid, objc_l, pgh_l, hmask);
-        else if constexpr (kHCap >= 64)
-          h_cols_lane<64>(update, grad_valid, objc_l, pgh_l, hmask);
+        else if constexpr (kHCap >= 64) {
+          // k <= 48 (C4: k = 40): a 48-long register array instead of 64 -- the unrolled j loops issue
+          // their predicated-off tail too, a quarter of the phase's DFMA / LDS slots at k = 40
+          if (k <= 48)
+            h_cols_lane<48>(update, grad_valid, objc_l, pgh_l, hmask);
+          else
+            h_cols_lane<64>(update, grad_valid, objc_l, pgh_l, hmask);
+        }
       }
     } else
     for (int64_t cb = int64_t(wid) * CPW; cb < NC; cb += int64_t(kSwWarps) * CPW) {

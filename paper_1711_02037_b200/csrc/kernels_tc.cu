@@ -306,7 +306,12 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xw_kern
       uint32_t it = 0;
       // 3xTF32: only the raw S^T slab comes from L2 and the split warps write its lo slab on chip;
       // LT: the split warps only handle X, the lo slab comes by TMA
-      const uint32_t bytes = uint32_t(kXTileBytes + C::kSBytes * (LT ? 2 : 1));
+#ifdef RNMF_TC_XW_SLO_ONCHIP  // (experiment) LT with the S^T lo slab split on chip, as X^T S does
+      constexpr bool kSloTma = false;
+#else
+      constexpr bool kSloTma = LT;
+#endif
+      const uint32_t bytes = uint32_t(kXTileBytes + C::kSBytes * (kSloTma ? 2 : 1));
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = int(it % S);
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xw_kern
           tc::mbar_arrive_expect_tx(&sm.full[s], bytes);
           tc::tma_load_2d_hint(sm.x(s), &tmX, &sm.full[s], kc * kBK, int(t * kBM), kXPolicy);
           tc::tma_load_2d_hint(sm.shi(s), &tmShi, &sm.full[s], kc * kBK, 0, kSPolicy);
-          if (LT) tc::tma_load_2d_hint(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0, kSPolicy);
+          if (kSloTma) tc::tma_load_2d_hint(sm.slo(s), &tmSlo, &sm.full[s], kc * kBK, 0, kSPolicy);
         }
       }
     }
@@ -436,6 +441,11 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xw_kern
           tc::tc_fence_after();
 #ifndef RNMF_TC_DBG_NOSPLIT
           lt_store16(tmem_base + lane_off + uint32_t(C::kLoBase + s * kBK + half * 16), v);
+#ifdef RNMF_TC_XW_SLO_ONCHIP
+          split_lo_tile<C::kSBytes / 16, 256>(reinterpret_cast<const float4*>(sm.shi(s)),
+                                              reinterpret_cast<float4*>(sm.slo(s)), (quad * 2 + half) * 32 + lane);
+          tc::fence_proxy_async_smem();
+#endif
 #endif
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&sm.lofull[s]);
@@ -1685,12 +1695,17 @@ struct FwCfg {
   static constexpr int kHtBytes = 2 * (2 * 32 * 128);  // 2 K atoms x (hi | lo)
   static constexpr int kStageBytes = kXTileBytes + 2 * kSBytes + kHtBytes;
   static constexpr int kLoW = 2;
-  static constexpr int kLoBytes = kLoW * kXTileBytes;
+  // kLT (k <= 48): the lo X tiles live in tensor memory (kLoW x 32 columns, written by four split
+  // warps with tcgen05.st; the small-term UMMA takes A from TMEM) instead of a shared-memory ring,
+  // which buys one more TMA stage; the W H ring is then two slots deep.  TMEM is full either way.
+  static constexpr bool kLT = NPAD <= 48;
+  static constexpr int kLoBytes = kLT ? 0 : kLoW * kXTileBytes;
   static constexpr int kStages = std::min(6, (226 * 1024 - kLoBytes - 2048) / kStageBytes);
   static constexpr int kAccCols = 2 * NPAD;
   static constexpr int kRsBase = 2 * kAccCols;
-  static constexpr int kRb = (512 - kRsBase - 128) / 64;  // W H ring depth
-  static constexpr int kWBase = kRsBase + kRb * 64;
+  static constexpr int kRb = kLT ? 2 : (512 - kRsBase - 128) / 64;  // W H ring depth
+  static constexpr int kLoT = kRsBase + kRb * 64;                    // TMEM lo ring (kLT)
+  static constexpr int kWBase = kLoT + (kLT ? kLoW * kBK : 0);
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kLoBytes + 1024 + 512;
   static_assert(kStages >= 3 && kRb >= 2 && kWBase + 128 <= 512, "layout");
 };
@@ -1735,7 +1750,7 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
       tc::mbar_init(&empty[s], 1 + 128);
     }
     for (int j = 0; j < LO; ++j) {
-      tc::mbar_init(&lofull[j], kSplitThreads);
+      tc::mbar_init(&lofull[j], C::kLT ? 128 : kSplitThreads);
       tc::mbar_init(&loempty[j], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -1817,7 +1832,11 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
             tc::umma_tf32_w(d, xa + 2 * k, kHi, ba + 2 * k, kHi, idesc2, (kin == 0 && k == 0) ? 0u : 1u);  // X_hi [S_hi; S_lo]
-            tc::umma_tf32_w(d + NPAD, la + 2 * k, kHi, ba + 2 * k, kHi, idesc1, 1u);                       // += X_lo S_hi
+            if (C::kLT)  // += X_lo S_hi, A from tensor memory
+              tc::umma_tf32_ts_w(d + NPAD, tmem_base + uint32_t(C::kLoT) + j * uint32_t(kBK) + uint32_t(8 * k), ba + 2 * k,
+                                 kHi, idesc1, 1u);
+            else
+              tc::umma_tf32_w(d + NPAD, la + 2 * k, kHi, ba + 2 * k, kHi, idesc1, 1u);
           }
           const uint32_t dr = tmem_base + uint32_t(C::kRsBase) + b * 64u;
           const uint32_t ha = ba + uint32_t((2 * C::kSBytes) >> 4);  // H^T slab: two 32-wide K atoms of (hi | lo) rows
@@ -1845,6 +1864,42 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
       }
     }
   } else if (warp < 4 || warp >= 8) {
+    if constexpr (C::kLT) {
+      // warps 8..11 (TMEM lane quadrants 0..3): lo of the thread's X row -> the TMEM lo slot
+      if (warp >= 8) {
+        const int quad = warp & 3, r = quad * 32 + lane;
+        const uint32_t lane_off = uint32_t(quad * 32) << 16;
+        uint32_t it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+          for (int kc = 0; kc < nk; ++kc, ++it) {
+            const int s = int(it % S), j = int(it % LO);
+            tc::mbar_wait(&full[s], (it / S) & 1);
+            const uint32_t xrow = tc::smem_u32(xst(s)) + uint32_t(r) * 128u;
+            uint32_t v0[16], v1[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v0[4 * c]), "=r"(v0[4 * c + 1]), "=r"(v0[4 * c + 2]), "=r"(v0[4 * c + 3])
+                           : "r"(xrow + uint32_t((c ^ (r & 7)) * 16)) : "memory");
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v1[4 * c]), "=r"(v1[4 * c + 1]), "=r"(v1[4 * c + 2]), "=r"(v1[4 * c + 3])
+                           : "r"(xrow + uint32_t(((4 + c) ^ (r & 7)) * 16)) : "memory");
+            }
+            tc::mbar_wait(&loempty[j], ((it / LO) & 1) ^ 1);
+            tc::tc_fence_after();
+            uint32_t r0[16], r1[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r0[i] = tf32_lo_bits(v0[i]), r1[i] = tf32_lo_bits(v1[i]);
+            const uint32_t ta = tmem_base + lane_off + uint32_t(C::kLoT + j * kBK);
+            tc::tmem_st_32x32b_x16(ta, r0);
+            tc::tmem_st_32x32b_x16(ta + 16, r1);
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            tc::mbar_arrive(&lofull[j]);
+          }
+        }
+      }
+    } else {
     const int st = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;
     uint32_t it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -1856,6 +1911,7 @@ __global__ void __launch_bounds__(kTcThreadsX3, 1) tc_xht_resid_w_kernel(
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&lofull[j]);
       }
+    }
     }
   } else {
     const int sub = warp & 3;
