@@ -505,6 +505,18 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xw_kern
   }
 }
 
+// Work unit u -> (column tile, row split).  Split-major: the CTAs running at one time take the
+// column tiles of ONE row split, so the S^T rows they re-read are one split's (l x m / splits:
+// 6 MB at C4 instead of all 51 MB) and neighbouring CTAs read adjacent 512-byte segments of the same
+// X rows.  RNMF_TC_XTW_TILE_MAJOR restores the round-1 order (u = tile * splits + split).
+#ifdef RNMF_TC_XTW_TILE_MAJOR
+#define RNMF_XTW_UNIT_CT(u) ((u) / p.splits)
+#define RNMF_XTW_UNIT_SPLIT(u) ((u) % p.splits)
+#else
+#define RNMF_XTW_UNIT_CT(u) ((u) % ctiles)
+#define RNMF_XTW_UNIT_SPLIT(u) ((u) / ctiles)
+#endif
+
 // ------------------------------------------------------------------------------------------------
 // tc_xtw: part[split] (n x c) = X[rows of split]^T (n x m_s) * S[rows of split] (m_s x c)
 //   A = X^T tile: M = 128 X columns (MN-major: four 32-column TMA boxes, LBO = 4 KB),
@@ -546,7 +558,7 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_ker
   // split boundaries on 32-row stage boundaries, so no stage straddles two splits
   const int64_t mstages = ceil_div(p.m, kBK);
   auto unit_rows = [&](int64_t u, int64_t& r0, int64_t& r1) {
-    const int64_t sp = u % p.splits;
+    const int64_t sp = RNMF_XTW_UNIT_SPLIT(u);
     r0 = (mstages * sp / p.splits) * kBK;
     r1 = (mstages * (sp + 1) / p.splits) * kBK;
   };
@@ -555,7 +567,7 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_ker
     if (tc::elect_one()) {
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int64_t ct = u / p.splits;
+        const int64_t ct = RNMF_XTW_UNIT_CT(u);
         int64_t r0, r1;
         unit_rows(u, r0, r1);
         for (int64_t r = r0; r < r1; r += kBK, ++it) {
@@ -732,7 +744,7 @@ __global__ void __launch_bounds__((TcCfg<NPAD, X3, LT>::kThreads), 1) tc_xtw_ker
     const int sub = warp & 3;
     uint32_t ci = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const int64_t ct = u / p.splits, sp = u % p.splits;
+      const int64_t ct = RNMF_XTW_UNIT_CT(u), sp = RNMF_XTW_UNIT_SPLIT(u);
       int64_t r0, r1;
       unit_rows(u, r0, r1);
       const int64_t nst = (r1 - r0) / kBK;
