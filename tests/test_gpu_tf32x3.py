@@ -93,12 +93,14 @@ def test_tf32x3_edge_shapes(gpu, oracle, m, n, k):
     assert abs(res.trace[-1].rel_err - ref.trace[-1]["rel_err"]) <= 1e-4 + 1e-3 * ref.trace[-1]["rel_err"]
 
 
-@pytest.mark.parametrize("m,n,k,p", [(20000, 3000, 40, 20), (30011, 777, 16, 20), (9000, 5000, 10, 6)])
+@pytest.mark.parametrize("m,n,k,p", [(20000, 3000, 40, 20), (30011, 777, 16, 20), (9000, 5000, 10, 6), (6000, 4000, 64, 32),
+                                     (12000, 2500, 33, 15)])
 def test_tf32x3_bitwise_repeatable(gpu, m, n, k, p):
     """Three fits of the same inputs give identical bits (W, H and every trace field).  The
     tensor-core kernels hand tiles between the TMA, split, UMMA and epilogue warps through
     mbarriers and tensor memory; a missed wait or a slot reused too early would show up here as
-    run-to-run differences.  Shapes: many persistent tiles per CTA, ragged tails, l = 60 / 36 / 16."""
+    run-to-run differences.  Shapes: many persistent tiles per CTA, ragged tails, l = 60 / 36 / 16 / 96 / 48
+    (tensor-memory and shared-memory lo layouts, both fused metrics kernels)."""
     x = workloads.noisy_lowrank_matrix(3, m, n, k, 0.5, 0.1)
     o = gpu.SolverOptions(rank=k, max_iter=12, tol=1e-300, oversampling=p, power_iterations=2, seed=5,
                           trace_full_every=3)
