@@ -15,7 +15,7 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
 echo "launch list rc=$?"
 timeout 300 python tools/run_fit.py --config $CFG --fits 1 > $OUT/fit.json 2>&1 || { echo "fit failed"; exit 1; }
 for K in rhals_sweeps_kernel tc_xht_resid_w_kernel tc_xw_kernel tc_xtw_kernel; do
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none -k regex:$K -s 1 -c 1 \
     -o $OUT/${K}_${CFG} python tools/run_fit.py --config $CFG --fits 1 > $OUT/ncu_${K}.log 2>&1
   echo "ncu $K rc=$?"
 done
